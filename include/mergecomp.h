@@ -1,0 +1,132 @@
+/*
+ * mergecomp.h — C ABI of the B200-native MergeComp compressed gradient-sync path.
+ *
+ * Drop-in boundary for the reference's codec module
+ * (/root/reference/pkg/src/mergesched/compressors.py).  Every entry point is
+ * extern "C", takes plain pointers and sizes (device pointers unless stated),
+ * returns an int status (MC_OK = 0, negative on argument/CUDA errors) and never
+ * throws.  All device work is stream-ordered on the caller's cudaStream_t
+ * (passed as void*); the library keeps no global mutable state except a cached
+ * SM count.  Data-dependent errors (non-finite gradients, corrupt indices) are
+ * OR-ed into a caller-owned device word `err_flags` and surface at the
+ * caller's next sync point, where the Python layer raises the reference's
+ * ValueError.
+ *
+ * Reference interface each entry point replaces:
+ *   mc_top_k_count        <- top_k_count            compressors.py:185-194
+ *   mc_payload_bytes      <- payload_bytes          compressors.py:565-596
+ *   mc_derive_seed        <- derive_seed            compressors.py:247-251
+ *   mc_encode             <- encode (+ _compress)   compressors.py:369-417, 259-366
+ *   mc_decode_mean        <- aggregate (+ decode)   compressors.py:519-532, 427-516
+ *   mc_pack / mc_unpack   <- Trainer._group_slices  trainer.py:344-348 (merge stage)
+ *   mc_serialize          <- serialize              compressors.py:601-620
+ */
+#ifndef MERGECOMP_H
+#define MERGECOMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MC_ABI_VERSION 1
+
+/* status codes */
+#define MC_OK 0
+#define MC_EINVAL (-1)       /* bad argument (null pointer, n < 1, bad spec) */
+#define MC_ECUDA (-2)        /* a CUDA launch or runtime call failed */
+#define MC_EWORKSPACE (-3)   /* workspace smaller than mc_encode_workspace_bytes() */
+
+/* device error flags, OR-ed into *err_flags */
+#define MC_ERR_NONFINITE 0x1u    /* "gradient contains non-finite values"   compressors.py:384-385 */
+#define MC_ERR_INDEX_RANGE 0x2u  /* "corrupt payload: index out of range"   compressors.py:444 */
+#define MC_ERR_INDEX_ORDER 0x4u  /* "corrupt payload: indices not increasing" compressors.py:445 */
+#define MC_ERR_HEADER 0x8u       /* payload header does not match spec / length */
+
+/* algorithm ids == position in the reference ALGORITHMS tuple (compressors.py:29-43) */
+enum {
+  MC_IDENTITY = 0, MC_FP16 = 1, MC_TOPK = 2, MC_RANDK = 3, MC_DGC_LITE = 4,
+  MC_THRESHOLD = 5, MC_QSGD = 6, MC_SIGNSGD = 7, MC_EFSIGNSGD = 8, MC_ONEBIT = 9,
+  MC_SIGNUM = 10, MC_TERNGRAD = 11, MC_INT8 = 12, MC_NUM_ALGORITHMS = 13
+};
+
+/* Resolved CompressorSpec (compressors.py:58-107): defaults already folded in. */
+typedef struct mc_spec {
+  int32_t algorithm;        /* MC_* id */
+  int32_t levels;           /* qsgd lattice size (>= 2) */
+  int64_t bucket_size;      /* elements per scaling bucket (>= 1) */
+  double sparsity;          /* dropped fraction for k-sparsifiers, [0, 1) */
+  double threshold;         /* threshold codec tau (>= 0) */
+  int32_t error_feedback;   /* CompressorSpec.uses_error_feedback */
+  int32_t unbiased_scaling; /* randk x (n/k) */
+  int32_t has_momentum;     /* CompressorSpec.momentum_coef is not None */
+  float momentum;           /* float32(momentum_coef) */
+} mc_spec;
+
+/* Device payload: a 32-byte header followed by 16-byte aligned sections.
+ *   idx   u32[cap]      sparsifier indices, ascending
+ *   val   f32[n_val]    selected values / bucket scalers (sparse: capacity cap)
+ *   bits  u8[n_bits]    sign bits (MSB-first) / packed ternary codes / fp16 / int8
+ *   codes u8[n_codes]   qsgd level codes (MSB-first, width = bit_length(levels-1))
+ * The canonical 22-byte-header wire form of the reference is produced by
+ * mc_serialize; the aligned form is what moves through NCCL. */
+typedef struct mc_payload_header {
+  uint32_t algorithm;
+  uint32_t flags;           /* 0x01 = randk unbiased scaling (compressors.py:55) */
+  uint64_t original_len;
+  uint32_t n_idx;           /* selected count (sparsifiers), else 0 */
+  uint32_t n_val;
+  uint32_t n_bits;          /* canonical bits length (signs + codes for qsgd) */
+  uint32_t cap;             /* idx/val capacity of this buffer (sparsifiers) */
+} mc_payload_header;
+
+typedef struct mc_layout {
+  int64_t n;
+  int64_t cap;              /* sparse capacity (k, or n for threshold), 0 if dense */
+  int64_t n_val, n_bits, n_codes;
+  int64_t off_idx, off_val, off_bits, off_codes;
+  int64_t bytes;            /* total device payload size, multiple of 16 */
+} mc_layout;
+
+int mc_abi_version(void);
+const char* mc_last_error(void); /* thread-local message of the last failing call */
+
+int64_t mc_top_k_count(double sparsity, int64_t n);
+int64_t mc_payload_bytes(const mc_spec* spec, int64_t n);               /* canonical, incl. 22-B header */
+int mc_payload_layout(const mc_spec* spec, int64_t n, int64_t cap, mc_layout* out); /* cap<=0: default */
+int64_t mc_encode_workspace_bytes(const mc_spec* spec, int64_t n);
+
+/* SeedSequence(entropy=(root, worker, iteration, group)).generate_state(2, u64) */
+int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t group,
+                   uint64_t* key_lo, uint64_t* key_hi);
+
+/* Encode one group of n fp32 gradients into `payload` (device, >= layout.bytes).
+ * residual (f64[n]) must be non-null iff spec->error_feedback; momentum (f32[n])
+ * iff spec->has_momentum.  Both are updated in place.  (key_lo, key_hi) is the
+ * 128-bit Philox key of derive_seed() for the stochastic codecs. */
+int mc_encode(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+              uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
+              uint32_t* err_flags, void* stream);
+
+/* out[i] = (sum_{r=0..nranks-1} decode(payload_r)[i]) / f32(nranks), summed in rank
+ * order in fp32 exactly as aggregate().  Payload r lives at payloads + r*stride_bytes. */
+int mc_decode_mean(const mc_spec* spec, const void* payloads, int64_t stride_bytes, int32_t nranks,
+                   int64_t n, float* out, uint32_t* err_flags, void* stream);
+
+/* Merge stage: gather `count` device tensors (host array of device pointers)
+ * into one contiguous buffer in list order / scatter it back. */
+int mc_pack(const float* const* srcs, const int64_t* numels, int32_t count, float* fused, void* stream);
+int mc_unpack(const float* fused, float* const* dsts, const int64_t* numels, int32_t count, void* stream);
+
+/* Canonical little-endian byte form of a device payload into device `out`
+ * (capacity out_cap bytes); *out_len (host) receives the byte length.  Synchronises
+ * the stream for data-dependent (threshold) payloads. */
+int mc_serialize(const mc_spec* spec, const void* payload, int64_t n, void* out, int64_t out_cap,
+                 int64_t* out_len, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MERGECOMP_H */

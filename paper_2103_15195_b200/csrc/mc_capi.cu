@@ -1,0 +1,375 @@
+// mc_capi.cu — the extern "C" boundary (include/mergecomp.h): argument validation,
+// payload layout, SeedSequence key derivation and dispatch to the codec kernels.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "mc_internal.cuh"
+
+namespace mc {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached = v;
+  }
+  return cached;
+}
+
+// max(1, ceil(round((1 - s) * n, 9)))  — compressors.py:185-194.  Python's round(x, 9)
+// is the correctly rounded decimal at 9 places; glibc printf("%.9f") is too.
+int64_t top_k_count(double sparsity, int64_t n) {
+  if (n < 1) return -1;
+  char buf[64];
+  snprintf(buf, sizeof(buf), "%.9f", (1.0 - sparsity) * (double)n);
+  const double v = strtod(buf, nullptr);
+  const int64_t k = (int64_t)std::ceil(v);
+  return k < 1 ? 1 : k;
+}
+
+static bool spec_ok(const mc_spec* s) {
+  if (!s) { set_error("null spec"); return false; }
+  if (s->algorithm < 0 || s->algorithm >= MC_NUM_ALGORITHMS) { set_error("unknown algorithm id %d", s->algorithm); return false; }
+  if (!(s->sparsity >= 0.0 && s->sparsity < 1.0)) { set_error("sparsity must be in [0, 1)"); return false; }
+  if (s->levels < 2) { set_error("levels must be >= 2"); return false; }
+  if (s->bucket_size < 1) { set_error("bucket_size must be >= 1"); return false; }
+  if (s->threshold < 0) { set_error("threshold must be >= 0"); return false; }
+  return true;
+}
+
+// Device payload layout (see mc_payload_header in include/mergecomp.h).
+int fill_layout(const mc_spec* s, int64_t n, int64_t cap, mc_layout* L) {
+  if (!spec_ok(s) || n < 1 || !L) { if (n < 1) set_error("n must be >= 1"); return MC_EINVAL; }
+  memset(L, 0, sizeof(*L));
+  L->n = n;
+  const int64_t nb = cdiv(n, s->bucket_size);
+  const int64_t sb = cdiv(n, 8);
+  const int a = s->algorithm;
+  if (is_sparse(a)) {
+    int64_t k = top_k_count(s->sparsity, n);
+    if (a == MC_THRESHOLD) k = cap > 0 ? cap : n;
+    L->cap = k;
+    L->n_val = k;
+    L->off_idx = HDR;
+    L->off_val = HDR + a16(4 * k);
+    L->off_bits = L->off_val + a16(4 * k);
+    L->off_codes = L->off_bits;
+    L->bytes = L->off_codes;
+    return MC_OK;
+  }
+  switch (a) {
+    case MC_IDENTITY: L->n_val = n; break;
+    case MC_FP16: L->n_bits = 2 * n; break;
+    case MC_QSGD: L->n_val = nb; L->n_bits = sb; L->n_codes = cdiv(n * (int64_t)level_bits(s->levels), 8); break;
+    case MC_SIGNSGD:
+    case MC_SIGNUM: L->n_val = 1; L->n_bits = sb; break;
+    case MC_EFSIGNSGD: L->n_val = nb; L->n_bits = sb; break;
+    case MC_ONEBIT: L->n_val = 2 * nb; L->n_bits = sb; break;
+    case MC_TERNGRAD: L->n_val = nb; L->n_bits = cdiv(2 * n, 8); break;
+    case MC_INT8: L->n_val = nb; L->n_bits = n; break;
+  }
+  L->off_idx = HDR;
+  L->off_val = HDR;
+  L->off_bits = L->off_val + a16(4 * L->n_val);
+  L->off_codes = L->off_bits + a16(L->n_bits);
+  L->bytes = L->off_codes + a16(L->n_codes);
+  return MC_OK;
+}
+
+// ---------------------------------------------------------------- numpy SeedSequence
+namespace seedseq {
+constexpr uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u, INIT_B = 0x8b51f9ddu, MULT_B = 0x58f38dedu;
+constexpr uint32_t MIX_L = 0xca01f9ddu, MIX_R = 0x4973f715u;
+static uint32_t hashmix(uint32_t v, uint32_t& hc) {
+  v ^= hc;
+  hc *= MULT_A;
+  v *= hc;
+  v ^= v >> 16;
+  return v;
+}
+static uint32_t mix(uint32_t x, uint32_t y) {
+  uint32_t r = MIX_L * x - MIX_R * y;
+  r ^= r >> 16;
+  return r;
+}
+}  // namespace seedseq
+
+}  // namespace mc
+
+using namespace mc;
+
+extern "C" {
+
+int mc_abi_version(void) { return MC_ABI_VERSION; }
+const char* mc_last_error(void) { return g_err; }
+
+int64_t mc_top_k_count(double sparsity, int64_t n) { return top_k_count(sparsity, n); }
+
+int64_t mc_payload_bytes(const mc_spec* s, int64_t n) {
+  if (!spec_ok(s) || n < 1) return MC_EINVAL;
+  const int64_t nb = cdiv(n, s->bucket_size), sb = cdiv(n, 8);
+  const int64_t H = 22;
+  switch (s->algorithm) {
+    case MC_IDENTITY: return H + 4 * n;
+    case MC_FP16: return H + 2 * n;
+    case MC_TOPK: case MC_RANDK: case MC_DGC_LITE: case MC_THRESHOLD: return H + 8 * top_k_count(s->sparsity, n);
+    case MC_QSGD: return H + 4 * nb + sb + cdiv(n * (int64_t)level_bits(s->levels), 8);
+    case MC_SIGNSGD: case MC_SIGNUM: return H + 4 + sb;
+    case MC_EFSIGNSGD: return H + 4 * nb + sb;
+    case MC_ONEBIT: return H + 8 * nb + sb;
+    case MC_TERNGRAD: return H + 4 * nb + cdiv(2 * n, 8);
+    case MC_INT8: return H + 4 * nb + n;
+  }
+  return MC_EINVAL;
+}
+
+int mc_payload_layout(const mc_spec* s, int64_t n, int64_t cap, mc_layout* out) { return fill_layout(s, n, cap, out); }
+
+int64_t mc_encode_workspace_bytes(const mc_spec* s, int64_t n) {
+  if (!spec_ok(s) || n < 1) return MC_EINVAL;
+  switch (s->algorithm) {
+    case MC_IDENTITY: case MC_FP16: return 64;
+    case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: return bucket_ws_bytes(s, n);
+    case MC_SIGNSGD: case MC_SIGNUM: return signglobal_ws_bytes(s, n);
+    default: return sparse_ws_bytes(s, n);
+  }
+}
+
+int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t group, uint64_t* key_lo,
+                   uint64_t* key_hi) {
+  using namespace seedseq;
+  if (!key_lo || !key_hi) { set_error("null output"); return MC_EINVAL; }
+  uint32_t ent[8];
+  int ne = 0;
+  const uint64_t in[4] = {root, worker, iteration, group};
+  for (int i = 0; i < 4; ++i) {  // _coerce_to_uint32_array: 0 -> [0], else little-endian 32-bit words
+    uint64_t v = in[i];
+    if (v == 0) { ent[ne++] = 0; continue; }
+    while (v) { ent[ne++] = (uint32_t)(v & 0xffffffffu); v >>= 32; }
+  }
+  uint32_t pool[4];
+  uint32_t hc = INIT_A;
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < ne ? ent[i] : 0u, hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s], hc));
+  for (int s = 4; s < ne; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[s], hc));
+  uint32_t st[4];
+  uint32_t hb = INIT_B;
+  for (int i = 0; i < 4; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= MULT_B;
+    v *= hb;
+    v ^= v >> 16;
+    st[i] = v;
+  }
+  *key_lo = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+  *key_hi = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+  return MC_OK;
+}
+
+int mc_encode(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum, uint64_t key_lo,
+              uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+              void* stream) {
+  if (!spec_ok(s)) return MC_EINVAL;
+  if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
+  if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
+  if (s->error_feedback && !residual) { set_error("error feedback requires a residual buffer"); return MC_EINVAL; }
+  if (s->has_momentum && !momentum) { set_error("momentum codec requires a momentum buffer"); return MC_EINVAL; }
+  if (n > 0x7fffffffLL) { set_error("group length must be < 2^31"); return MC_EINVAL; }
+  const int64_t need = mc_encode_workspace_bytes(s, n);
+  if (workspace_bytes < need || (need > 64 && !workspace)) {
+    set_error("workspace %lld < required %lld", (long long)workspace_bytes, (long long)need);
+    return MC_EWORKSPACE;
+  }
+  EncodeArgs a{};
+  a.spec = s;
+  if (fill_layout(s, n, 0, &a.L) != MC_OK) return MC_EINVAL;
+  a.g = grad;
+  a.n = n;
+  a.r = residual;
+  a.m = momentum;
+  a.k0 = key_lo;
+  a.k1 = key_hi;
+  a.payload = static_cast<uint8_t*>(payload);
+  a.ws = static_cast<uint8_t*>(workspace);
+  a.ws_bytes = workspace_bytes;
+  a.ctx.stream = static_cast<cudaStream_t>(stream);
+  a.ctx.err = err_flags;
+  switch (s->algorithm) {
+    case MC_IDENTITY: case MC_FP16: return encode_elementwise(a);
+    case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: return encode_bucketed(a);
+    case MC_SIGNSGD: case MC_SIGNUM: return encode_sign_global(a);
+    case MC_TOPK: case MC_DGC_LITE: return encode_topk(a);
+    case MC_RANDK: return encode_randk(a);
+    case MC_THRESHOLD: return encode_threshold(a);
+  }
+  return MC_EINVAL;
+}
+
+int mc_decode_mean(const mc_spec* s, const void* payloads, int64_t stride_bytes, int32_t nranks, int64_t n, float* out,
+                   uint32_t* err_flags, void* stream) {
+  if (!spec_ok(s)) return MC_EINVAL;
+  if (n < 1 || nranks < 1 || !payloads || !out || !err_flags) { set_error("bad decode arguments"); return MC_EINVAL; }
+  if (nranks > 1 && stride_bytes < 32) { set_error("stride too small"); return MC_EINVAL; }
+  mc_layout L;
+  if (fill_layout(s, n, 0, &L) != MC_OK) return MC_EINVAL;
+  Ctx c{static_cast<cudaStream_t>(stream), err_flags};
+  const uint8_t* base = static_cast<const uint8_t*>(payloads);
+  if (is_sparse(s->algorithm)) return decode_mean_sparse(s, L, base, stride_bytes, nranks, out, c);
+  return decode_mean_dense(s, L, base, stride_bytes, nranks, out, c);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- merge stage + serialize
+namespace mc {
+namespace {
+
+constexpr int PACK_MAX = 128;
+struct PackArgs {
+  const float* src[PACK_MAX];
+  float* dst[PACK_MAX];
+  int64_t off[PACK_MAX + 1];  // element offset of tensor i inside the fused buffer
+  int count;
+  int to_fused;  // 1: pack (tensors -> fused), 0: unpack (fused -> tensors)
+  float* fused;
+  const float* cfused;
+};
+
+__global__ void k_pack(PackArgs a) {
+  const int64_t total = a.off[a.count];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = a.count - 1;  // tensor holding element e: largest i with off[i] <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int64_t j = e - a.off[lo];
+    if (a.to_fused) a.fused[e] = a.src[lo][j];
+    else a.dst[lo][j] = a.cfused[e];
+  }
+}
+
+int pack_impl(const float* const* srcs, float* const* dsts, const int64_t* numels, int32_t count, float* fused,
+              const float* cfused, int to_fused, cudaStream_t st) {
+  if (count < 0 || !numels || (count > 0 && (to_fused ? !srcs : !dsts))) { set_error("bad pack arguments"); return MC_EINVAL; }
+  int64_t base = 0;
+  for (int32_t i0 = 0; i0 < count; i0 += PACK_MAX) {
+    PackArgs a{};
+    a.count = (int)imin(PACK_MAX, count - i0);
+    a.to_fused = to_fused;
+    a.off[0] = 0;
+    for (int i = 0; i < a.count; ++i) {
+      if (numels[i0 + i] < 0) { set_error("negative numel"); return MC_EINVAL; }
+      if (to_fused) a.src[i] = srcs[i0 + i]; else a.dst[i] = dsts[i0 + i];
+      a.off[i + 1] = a.off[i] + numels[i0 + i];
+    }
+    a.fused = fused ? fused + base : nullptr;
+    a.cfused = cfused ? cfused + base : nullptr;
+    const int64_t total = a.off[a.count];
+    if (total > 0) {
+      const unsigned grid = (unsigned)imax(1, imin(cdiv(total, 256), (int64_t)sm_count() * 8));
+      k_pack<<<grid, 256, 0, st>>>(a);
+      MC_LAUNCH_CHECK();
+    }
+    base += total;
+  }
+  return MC_OK;
+}
+
+struct SerArgs {
+  uint8_t header[24];
+  const uint8_t* src[4];
+  int64_t len[4];
+  int64_t start[5];  // output offsets of the 4 sections (start[0] = 22)
+  uint8_t* out;
+};
+
+__global__ void k_serialize(SerArgs a) {
+  const int64_t total = a.start[4];
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    if (o < 22) { a.out[o] = a.header[o]; continue; }
+    int s = 0;
+    while (s < 3 && o >= a.start[s + 1]) ++s;
+    a.out[o] = a.src[s][o - a.start[s]];
+  }
+}
+
+}  // namespace
+}  // namespace mc
+
+extern "C" {
+
+int mc_pack(const float* const* srcs, const int64_t* numels, int32_t count, float* fused, void* stream) {
+  if (!fused && count > 0) { set_error("null fused buffer"); return MC_EINVAL; }
+  return mc::pack_impl(srcs, nullptr, numels, count, fused, nullptr, 1, static_cast<cudaStream_t>(stream));
+}
+
+int mc_unpack(const float* fused, float* const* dsts, const int64_t* numels, int32_t count, void* stream) {
+  if (!fused && count > 0) { set_error("null fused buffer"); return MC_EINVAL; }
+  return mc::pack_impl(nullptr, dsts, numels, count, nullptr, fused, 0, static_cast<cudaStream_t>(stream));
+}
+
+int mc_serialize(const mc_spec* s, const void* payload, int64_t n, void* out, int64_t out_cap, int64_t* out_len,
+                 void* stream) {
+  mc_layout L;
+  if (fill_layout(s, n, 0, &L) != MC_OK) return MC_EINVAL;
+  if (!payload || !out || !out_len) { set_error("null pointer"); return MC_EINVAL; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  mc_payload_header h;
+  if (cudaMemcpyAsync(&h, payload, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("reading payload header failed");
+    return MC_ECUDA;
+  }
+  if ((int)h.algorithm != s->algorithm || h.original_len != (uint64_t)n) { set_error("payload header mismatch"); return MC_EINVAL; }
+  const uint8_t* p = static_cast<const uint8_t*>(payload);
+  SerArgs a{};
+  const int64_t nidx = h.n_idx, nval = h.n_val;
+  const bool sparse = is_sparse(s->algorithm);
+  a.src[0] = p + HDR;
+  a.len[0] = 4 * nidx;
+  a.src[1] = sparse ? p + HDR + a16(4 * (int64_t)h.cap) : p + L.off_val;
+  a.len[1] = 4 * nval;
+  a.src[2] = p + L.off_bits;
+  a.len[2] = sparse ? 0 : L.n_bits;
+  a.src[3] = p + L.off_codes;
+  a.len[3] = sparse ? 0 : L.n_codes;
+  a.start[0] = 22;
+  for (int i = 0; i < 4; ++i) a.start[i + 1] = a.start[i] + a.len[i];
+  const uint32_t nbits = (uint32_t)(a.len[2] + a.len[3]);
+  // "<BBQIII": algo u8, flags u8, original_len u64, n_idx u32, n_val u32, n_bits u32
+  a.header[0] = (uint8_t)h.algorithm;
+  a.header[1] = (uint8_t)h.flags;
+  memcpy(a.header + 2, &h.original_len, 8);
+  const uint32_t ni = (uint32_t)nidx, nv = (uint32_t)nval;
+  memcpy(a.header + 10, &ni, 4);
+  memcpy(a.header + 14, &nv, 4);
+  memcpy(a.header + 18, &nbits, 4);
+  a.out = static_cast<uint8_t*>(out);
+  *out_len = a.start[4];
+  if (out_cap < a.start[4]) { set_error("serialize buffer too small (%lld < %lld)", (long long)out_cap, (long long)a.start[4]); return MC_EINVAL; }
+  const unsigned grid = (unsigned)imax(1, imin(cdiv(a.start[4], 256), 4096));
+  k_serialize<<<grid, 256, 0, st>>>(a);
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// mc_dense.cu — identity / fp16 encode (compressors.py:265-270) and the fused
+// decode + rank-ordered mean for every dense codec (decode :450-514, aggregate :519-532).
+//
+// decode_mean: one thread owns 8 consecutive elements (one sign byte per rank); for
+// r = 0..nranks-1 it decodes payload r and accumulates acc = fl32(acc + d_r) starting
+// from +0.0f, then writes acc / f32(nranks) — the reference's float32 order exactly.
+#include "mc_internal.cuh"
+
+namespace mc {
+namespace {
+
+struct EP {
+  const float* g;
+  double* r;
+  int64_t n;
+  float* val;       // identity payload values
+  __half* half;     // fp16 payload
+  uint32_t* err;
+  uint8_t* payload;
+  mc_payload_header hdr;
+};
+
+template <int ALGO, bool EF>
+__global__ void k_elementwise(EP p) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
+  bool bad = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float x = p.g[e];
+    bad |= !isfinite(x);
+    double c = (double)x;
+    float c32 = x;
+    if (EF) {
+      c = __dadd_rn((double)x, p.r[e]);
+      c32 = __double2float_rn(c);
+    }
+    float dec;
+    if (ALGO == MC_IDENTITY) {
+      p.val[e] = c32;
+      dec = c32;
+    } else {
+      const __half h = __float2half_rn(c32);  // numpy astype(float16): RNE, overflow -> inf
+      p.half[e] = h;
+      dec = __half2float(h);
+    }
+    if (EF) p.r[e] = __dsub_rn(c, (double)dec);
+  }
+  flag(p.err, bad, MC_ERR_NONFINITE);
+}
+
+// ------------------------------------------------------------------ dense decode
+struct DP {
+  const uint8_t* base;
+  int64_t stride;
+  int nranks;
+  int64_t n, B;
+  int64_t off_val, off_bits, off_codes;
+  int width;
+  float top;
+  float inv_unused;
+  float* out;
+  uint32_t* err;
+  uint32_t algo;
+  uint32_t n_val, n_bits;
+};
+
+template <int ALGO>
+__device__ __forceinline__ float dec1(const DP& p, const uint8_t* pl, int64_t e) {
+  const float* val = reinterpret_cast<const float*>(pl + p.off_val);
+  const uint8_t* bits = pl + p.off_bits;
+  if (ALGO == MC_IDENTITY) return val[e];
+  if (ALGO == MC_FP16) return __half2float(reinterpret_cast<const __half*>(bits)[e]);
+  if (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) return __fmul_rn(sign_bit(bits, e) ? 1.0f : -1.0f, val[0]);
+  const int64_t b = e / p.B;
+  if (ALGO == MC_EFSIGNSGD) return __fmul_rn(sign_bit(bits, e) ? 1.0f : -1.0f, val[b]);
+  if (ALGO == MC_ONEBIT) return sign_bit(bits, e) ? val[2 * b + 1] : val[2 * b];
+  if (ALGO == MC_QSGD) {
+    const uint32_t code = read_code(pl + p.off_codes, e, p.width);
+    return __fmul_rn(__fmul_rn(sign_bit(bits, e) ? 1.0f : -1.0f, val[b]), __fdiv_rn((float)code, p.top));
+  }
+  if (ALGO == MC_TERNGRAD) {
+    const uint32_t code = (bits[e >> 2] >> (6 - 2 * (e & 3))) & 3u;
+    return __fmul_rn(__fsub_rn((float)code, 1.0f), val[b]);
+  }
+  /* MC_INT8 */ return __fmul_rn((float)(int8_t)bits[e], __fdiv_rn(val[b], 127.0f));
+}
+
+template <int ALGO>
+__global__ void k_decode_dense(DP p) {
+  if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
+    const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(p.base + p.stride * threadIdx.x);
+    if (h->algorithm != p.algo || h->original_len != (uint64_t)p.n || h->n_val != p.n_val || h->n_bits != p.n_bits)
+      atomicOr(p.err, MC_ERR_HEADER);
+  }
+  const float fn = (float)p.nranks;
+  const int64_t groups = cdiv(p.n, 8);
+  for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = gi * 8;
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+    for (int r = 0; r < p.nranks; ++r) {
+      const uint8_t* pl = p.base + p.stride * r;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (e0 + q < p.n) acc[q] = __fadd_rn(acc[q], dec1<ALGO>(p, pl, e0 + q));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], fn);
+    if (e0 + 7 < p.n && ((uintptr_t)(p.out + e0) % 16) == 0) {
+      reinterpret_cast<float4*>(p.out + e0)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      reinterpret_cast<float4*>(p.out + e0)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (e0 + q < p.n) p.out[e0 + q] = acc[q];
+    }
+  }
+}
+
+}  // namespace
+
+int encode_elementwise(const EncodeArgs& a) {
+  const mc_spec* s = a.spec;
+  EP p{};
+  p.g = a.g;
+  p.r = s->error_feedback ? a.r : nullptr;
+  p.n = a.n;
+  p.val = reinterpret_cast<float*>(a.payload + a.L.off_val);
+  p.half = reinterpret_cast<__half*>(a.payload + a.L.off_bits);
+  p.err = a.ctx.err;
+  p.payload = a.payload;
+  p.hdr.algorithm = (uint32_t)s->algorithm;
+  p.hdr.original_len = (uint64_t)a.n;
+  p.hdr.n_val = (uint32_t)a.L.n_val;
+  p.hdr.n_bits = (uint32_t)a.L.n_bits;
+  const unsigned grid = (unsigned)imin(cdiv(a.n, 256), (int64_t)sm_count() * 8);
+  cudaStream_t st = a.ctx.stream;
+  if (s->algorithm == MC_IDENTITY) {
+    if (p.r) k_elementwise<MC_IDENTITY, true><<<grid, 256, 0, st>>>(p);
+    else k_elementwise<MC_IDENTITY, false><<<grid, 256, 0, st>>>(p);
+  } else {
+    if (p.r) k_elementwise<MC_FP16, true><<<grid, 256, 0, st>>>(p);
+    else k_elementwise<MC_FP16, false><<<grid, 256, 0, st>>>(p);
+  }
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+
+int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks,
+                      float* out, const Ctx& c) {
+  DP p{};
+  p.base = base;
+  p.stride = stride;
+  p.nranks = nranks;
+  p.n = L.n;
+  p.B = s->bucket_size;
+  p.off_val = L.off_val;
+  p.off_bits = L.off_bits;
+  p.off_codes = L.off_codes;
+  p.width = level_bits(s->levels);
+  p.top = (float)(s->levels - 1);
+  p.out = out;
+  p.err = c.err;
+  p.algo = (uint32_t)s->algorithm;
+  p.n_val = (uint32_t)L.n_val;
+  p.n_bits = (uint32_t)(L.n_bits + L.n_codes);
+  const int64_t groups = cdiv(L.n, 8);
+  const unsigned grid = (unsigned)imax(1, imin(cdiv(groups, 256), (int64_t)sm_count() * 16));
+  cudaStream_t st = c.stream;
+#define MC_DEC_CASE(A) \
+  case A: k_decode_dense<A><<<grid, 256, 0, st>>>(p); break;
+  switch (s->algorithm) {
+    MC_DEC_CASE(MC_IDENTITY)
+    MC_DEC_CASE(MC_FP16)
+    MC_DEC_CASE(MC_SIGNSGD)
+    MC_DEC_CASE(MC_SIGNUM)
+    MC_DEC_CASE(MC_EFSIGNSGD)
+    MC_DEC_CASE(MC_ONEBIT)
+    MC_DEC_CASE(MC_QSGD)
+    MC_DEC_CASE(MC_TERNGRAD)
+    MC_DEC_CASE(MC_INT8)
+    default:
+      set_error("decode_mean_dense: algorithm %d is not dense", s->algorithm);
+      return MC_EINVAL;
+  }
+#undef MC_DEC_CASE
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+
+}  // namespace mc

@@ -1,0 +1,270 @@
+// mc_internal.cuh — shared device machinery of the sm_100a MergeComp kernels.
+//
+// Numerics contract: every float operation that the reference
+// performs in numpy is reproduced with an explicitly rounded intrinsic
+// (__fadd_rn/__fmul_rn/__fdiv_rn/__dadd_rn/...), the library is compiled with
+// --fmad=false and without fast-math, so results are bit-identical to the
+// numpy expressions cited at each use.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mergecomp.h"
+
+namespace mc {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int HDR = 32;  // sizeof(mc_payload_header)
+
+__host__ __device__ inline int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+__host__ __device__ inline int level_bits(int levels) {
+  int v = levels - 1, b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b < 1 ? 1 : b;
+}
+inline bool is_sparse(int a) { return a == MC_TOPK || a == MC_RANDK || a == MC_DGC_LITE || a == MC_THRESHOLD; }
+
+int64_t top_k_count(double sparsity, int64_t n);
+int fill_layout(const mc_spec* s, int64_t n, int64_t cap, mc_layout* L);
+int sm_count();
+void set_error(const char* fmt, ...);
+
+// --------------------------------------------------------------------------------------------
+// Per-call launch context.
+struct Ctx {
+  cudaStream_t stream;
+  uint32_t* err;
+};
+
+#define MC_LAUNCH_CHECK()                                                           \
+  do {                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) {                                                        \
+      ::mc::set_error("CUDA launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return MC_ECUDA;                                                              \
+    }                                                                               \
+  } while (0)
+
+// --------------------------------------------------------------------------------------------
+// Philox4x64-10, counter = (block + 1, 0, 0, 0): numpy's Philox bit generator
+// (Random123 round function).  Uniform double = (w >> 11) * 2^-53.
+struct Philox {
+  uint64_t k0, k1;
+  __device__ __forceinline__ void block(uint64_t blk, uint64_t out[4]) const {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+    uint64_t c0 = blk + 1, c1 = 0, c2 = 0, c3 = 0, a = k0, b = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      if (r) { a += W0; b += W1; }
+      const uint64_t lo0 = M0 * c0, hi0 = __umul64hi(M0, c0);
+      const uint64_t lo1 = M1 * c2, hi1 = __umul64hi(M1, c2);
+      c0 = hi1 ^ c1 ^ a; c1 = lo1; c2 = hi0 ^ c3 ^ b; c3 = lo0;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+  }
+};
+__device__ __forceinline__ double u53(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
+
+// --------------------------------------------------------------------------------------------
+// numpy float32 pairwise summation (umath loops_utils pairwise_sum):
+//   n < 8   : s = -0; s += a[i] sequentially
+//   n <= 128: 8 strided accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail
+//   else    : m = n/2 - (n/2)%8 ; P(a[:m]) + P(a[m:])
+// The ufunc reduce adds the result to a +0 identity, which callers apply.
+// Warp-cooperative, iterative post-order walk (identical control flow in all lanes);
+// `get(q)` returns element q of the sequence.  Result is valid in every lane.
+template <class Get>
+__device__ float warp_pairwise(const Get& get, int64_t L) {
+  const int lane = threadIdx.x & 31;
+  int64_t st_off[48], st_len[48];  // node stack; len < 0 marks "combine"
+  float vals[24];
+  int sp = 0, vp = 0;
+  st_off[sp] = 0; st_len[sp] = L; ++sp;
+  while (sp) {
+    --sp;
+    const int64_t off = st_off[sp], len = st_len[sp];
+    if (len < 0) {
+      const float b = vals[--vp], a = vals[--vp];
+      vals[vp++] = __fadd_rn(a, b);
+      continue;
+    }
+    if (len > 128) {
+      int64_t m = len / 2;
+      m -= m % 8;
+      st_off[sp] = 0; st_len[sp] = -1; ++sp;        // combine after both children
+      st_off[sp] = off + m; st_len[sp] = len - m; ++sp;
+      st_off[sp] = off; st_len[sp] = m; ++sp;       // left child processed first
+      continue;
+    }
+    float res;
+    if (len < 8) {
+      float s = -0.0f;
+      if (lane == 0)
+        for (int64_t q = 0; q < len; ++q) s = __fadd_rn(s, get(off + q));
+      res = __shfl_sync(FULL, s, 0);
+    } else {
+      const int64_t body = len - (len % 8);
+      float r = 0.0f;
+      if (lane < 8) {
+        r = get(off + lane);
+        for (int64_t i = 8; i < body; i += 8) r = __fadd_rn(r, get(off + i + lane));
+      }
+      r = __fadd_rn(r, __shfl_xor_sync(FULL, r, 1));
+      r = __fadd_rn(r, __shfl_xor_sync(FULL, r, 2));
+      r = __fadd_rn(r, __shfl_xor_sync(FULL, r, 4));
+      float s = r;
+      if (lane == 0)
+        for (int64_t q = body; q < len; ++q) s = __fadd_rn(s, get(off + q));
+      res = __shfl_sync(FULL, s, 0);
+    }
+    vals[vp++] = res;
+  }
+  return vals[0];
+}
+
+// numpy float32 mean of a sequence with a known pairwise sum:  f32( f64(0 + P) / n ).
+__device__ __forceinline__ float np_mean(float pairwise_sum, int64_t n) {
+  const float s = __fadd_rn(0.0f, pairwise_sum);
+  return __double2float_rn(__ddiv_rn((double)s, (double)n));
+}
+
+// --------------------------------------------------------------------------------------------
+// Decoupled look-back prefix scan across blocks (one 64-bit status word per block:
+// 2 flag bits | 62-bit value).  Blocks take tickets in launch order so every
+// predecessor is resident or finished — forward progress is guaranteed.
+constexpr uint64_t LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_MASK = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
+  return *reinterpret_cast<const volatile uint64_t*>(p);
+}
+__device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
+  *reinterpret_cast<volatile uint64_t*>(p) = v;
+}
+
+// Called by warp 0 of a block with its aggregate; returns the exclusive prefix in all lanes.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t bid, uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (bid == 0) {
+    if (lane == 0) { st_volatile(&status[0], LB_PRE | agg); }
+    return 0;
+  }
+  if (lane == 0) { st_volatile(&status[bid], LB_AGG | agg); }
+  __threadfence();
+  uint64_t prefix = 0;
+  int64_t j = bid - 1;
+  while (true) {
+    const int64_t idx = j - lane;
+    uint64_t s = LB_PRE;  // lanes past block 0 behave as an (empty) inclusive prefix
+    if (idx >= 0) {
+      do { s = ld_volatile(&status[idx]); } while ((s >> 62) == 0);
+    }
+    const unsigned pre = __ballot_sync(FULL, (s >> 62) == 2);
+    const int first = pre ? __ffs(pre) - 1 : 32;  // nearest inclusive prefix
+    uint64_t v = (lane <= first && idx >= 0) ? (s & LB_MASK) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    prefix += v;
+    if (pre) break;
+    j -= 32;
+  }
+  if (lane == 0) { st_volatile(&status[bid], LB_PRE | (prefix + agg)); }
+  return prefix;
+}
+
+// --------------------------------------------------------------------------------------------
+// Element prologue (compressors.py:381-411): non-finite check on the raw gradient,
+// momentum (signum: b*m + (1-b)*x ; dgc: b*m + x, two roundings, no FMA), error feedback
+// c = f64(work) + r (f64), c32 = f32(c).
+struct Prologue {
+  const float* g;
+  double* r;    // null unless EF
+  float* m;     // null unless momentum
+  float beta, omb;
+  int signum;
+  __device__ __forceinline__ double load(int64_t e, float& c32, bool& bad, bool update_mom) const {
+    const float x = g[e];
+    bad |= !isfinite(x);
+    float w = x;
+    if (m) {
+      const float mo = m[e];
+      w = signum ? __fadd_rn(__fmul_rn(beta, mo), __fmul_rn(omb, x)) : __fadd_rn(__fmul_rn(beta, mo), x);
+      if (update_mom) m[e] = w;
+    }
+    if (r) {
+      const double c = __dadd_rn((double)w, r[e]);
+      c32 = __double2float_rn(c);
+      return c;
+    }
+    c32 = w;
+    return (double)w;
+  }
+};
+
+__device__ __forceinline__ void flag(uint32_t* err, bool bad, uint32_t bit) {
+  const unsigned any = __ballot_sync(__activemask(), bad);
+  if (any && (threadIdx.x & 31) == __ffs(any) - 1) atomicOr(err, bit);
+}
+
+// Sign bit position helpers: element e lives in byte e>>3 at bit 7-(e&7) (np.packbits order).
+__device__ __forceinline__ uint32_t word_bit(int64_t e) { return 8u * ((e >> 3) & 3) + 7u - (e & 7); }
+__device__ __forceinline__ int sign_bit(const uint8_t* bits, int64_t e) { return (bits[e >> 3] >> (7 - (e & 7))) & 1; }
+
+// Reads code e (width w bits, MSB-first concatenation) from a packed byte stream.
+__device__ __forceinline__ uint32_t read_code(const uint8_t* p, int64_t e, int w) {
+  if (w == 8) return p[e];
+  const int64_t bit0 = e * (int64_t)w;
+  uint32_t v = 0;
+  for (int b = 0; b < w; ++b) {
+    const int64_t bit = bit0 + b;
+    v = (v << 1) | ((p[bit >> 3] >> (7 - (bit & 7))) & 1u);
+  }
+  return v;
+}
+
+// Device-side header writer.
+__device__ __forceinline__ void write_header(void* payload, uint32_t algo, uint32_t flags, uint64_t n, uint32_t n_idx,
+                                             uint32_t n_val, uint32_t n_bits, uint32_t cap) {
+  mc_payload_header* h = reinterpret_cast<mc_payload_header*>(payload);
+  h->algorithm = algo; h->flags = flags; h->original_len = n; h->n_idx = n_idx; h->n_val = n_val;
+  h->n_bits = n_bits; h->cap = cap;
+}
+
+// --------------------------------------------------------------------------------------------
+// Entry points implemented per codec family (host side of each .cu file).
+struct EncodeArgs {
+  const mc_spec* spec;
+  mc_layout L;
+  const float* g;
+  int64_t n;
+  double* r;
+  float* m;
+  uint64_t k0, k1;
+  uint8_t* payload;
+  uint8_t* ws;
+  int64_t ws_bytes;
+  Ctx ctx;
+};
+
+int64_t bucket_ws_bytes(const mc_spec* s, int64_t n);
+int64_t sparse_ws_bytes(const mc_spec* s, int64_t n);
+int64_t signglobal_ws_bytes(const mc_spec* s, int64_t n);
+
+int encode_elementwise(const EncodeArgs& a);   // identity, fp16
+int encode_bucketed(const EncodeArgs& a);      // qsgd, efsignsgd, onebit, terngrad, int8
+int encode_sign_global(const EncodeArgs& a);   // signsgd, signum
+int encode_topk(const EncodeArgs& a);          // topk, dgc_lite
+int encode_randk(const EncodeArgs& a);
+int encode_threshold(const EncodeArgs& a);
+
+int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks,
+                      float* out, const Ctx& c);
+int decode_mean_sparse(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks,
+                       float* out, const Ctx& c);
+
+}  // namespace mc

@@ -1,0 +1,78 @@
+"""Payload exchange between data-parallel ranks (the reference's in-memory list,
+trainer.py:377-389, becomes an allgather of device payload buffers).
+
+* fixed-size codecs: one ``all_gather_into_tensor`` of the aligned payload
+  buffer; rank r's payload lands at offset r * stride, which is exactly the
+  (base, stride, nranks) form mc_decode_mean consumes in rank order 0..n-1;
+* threshold (data-dependent count): counts are exchanged first, every rank
+  re-packs its payload with capacity = max count, then the padded buffers are
+  gathered.
+
+Device agnostic (NCCL on CUDA tensors in production, gloo on CPU tensors in the
+multi-process unit tests); world size 1 is a no-op view.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+HDR = 32  # sizeof(mc_payload_header)
+
+
+def _a16(x: int) -> int:
+    return (x + 15) & ~15
+
+
+def world(group=None) -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def allgather_fixed(payload: torch.Tensor, out: Optional[torch.Tensor] = None, group=None) -> tuple[torch.Tensor, int]:
+    """Gather equal-size uint8 payload buffers; returns (gathered, stride)."""
+    _, n = world(group)
+    stride = payload.numel()
+    if n == 1:
+        return payload, stride
+    if out is None:
+        out = torch.empty(n * stride, dtype=torch.uint8, device=payload.device)
+    dist.all_gather_into_tensor(out, payload, group=group)
+    return out, stride
+
+
+def read_count(payload: torch.Tensor) -> torch.Tensor:
+    """n_idx field of the device header (u32 at byte 16) as an int64 tensor on the payload's device."""
+    return payload[16:20].view(torch.int32).to(torch.int64)
+
+
+def _repack(payload: torch.Tensor, count: int, cap_out: int, cap_in: Optional[int]) -> torch.Tensor:
+    """Re-lay a sparse payload [hdr | idx[cap_in] | val[cap_in]] with capacity cap_out >= count."""
+    if cap_in is None:
+        cap_in = int(payload[28:32].view(torch.int32).cpu().item())
+    out = torch.zeros(HDR + 2 * _a16(4 * cap_out), dtype=torch.uint8, device=payload.device)
+    out[:HDR].copy_(payload[:HDR])
+    out[28:32].copy_(torch.tensor([cap_out], dtype=torch.int32).view(torch.uint8).to(payload.device))
+    out[HDR: HDR + 4 * count].copy_(payload[HDR: HDR + 4 * count])
+    v_in, v_out = HDR + _a16(4 * cap_in), HDR + _a16(4 * cap_out)
+    out[v_out: v_out + 4 * count].copy_(payload[v_in: v_in + 4 * count])
+    return out
+
+
+def allgather_variable(payload: torch.Tensor, group=None) -> tuple[torch.Tensor, int, list[int]]:
+    """Two-phase gather of sparse payloads with data-dependent counts.
+    Returns (gathered, stride, counts)."""
+    r, n = world(group)
+    cnt = read_count(payload)
+    if n == 1:
+        return payload, payload.numel(), [int(cnt.item())]
+    counts = torch.empty(n, dtype=torch.int64, device=payload.device)
+    dist.all_gather_into_tensor(counts, cnt, group=group)
+    counts_h = [int(v) for v in counts.cpu().tolist()]  # host sync: the padded size depends on it
+    cap = max(max(counts_h), 1)
+    mine = _repack(payload, counts_h[r], cap, None)
+    gathered, stride = allgather_fixed(mine, group=group)
+    return gathered, stride, counts_h

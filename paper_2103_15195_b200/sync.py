@@ -1,0 +1,196 @@
+"""The data-parallel sync engine: MergeComp's per-partition compressed gradient
+synchronisation on one rank (one process per GPU).
+
+It replaces the group loop of the reference ``Trainer.step``
+(trainer.py:376-389) and its timing handle (``timed_iteration`` /
+``pin_partition`` / ``tensor_profile``, trainer.py:325-336, 397-403):
+
+  merge    per-layer gradients live as views of ONE flat fp32 buffer in
+           backprop order, so every partition group is a contiguous slice and
+           the merge stage is zero-copy (mc_pack/mc_unpack exist for foreign
+           tensors);
+  encode   mc_encode on the group slice, EF residual / momentum state kept per
+           (partition.boundaries, group) exactly like trainer.py:380, Philox key
+           derive_seed(root, rank, iteration, group);
+  exchange NCCL allgather of the aligned payload (exchange.py);
+  decode   mc_decode_mean over the gathered payloads in rank order, written in
+           place into the group slice (= the averaged gradient);
+
+all on a dedicated side stream — the FIFO channel of the reference simulator
+(simulator.py:114-142).  Device error flags are checked lazily (``check()``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence, Union
+
+import torch
+
+from . import _native, exchange
+from .compressors import device_decode_mean, device_encode, split_seed
+from .profiles import LayerProfile, ModelProfile, Partition
+from .spec import CompressorSpec
+
+
+@dataclass
+class _Group:
+    start: int
+    end: int
+    layout: object
+    payload: torch.Tensor
+    gather: Optional[torch.Tensor]
+    residual: Optional[torch.Tensor]
+    momentum: Optional[torch.Tensor]
+
+    @property
+    def n(self) -> int:
+        return self.end - self.start
+
+
+class GradSync:
+    """Compressed gradient synchronisation for one rank.
+
+    ``grads`` (a list of per-layer views into ``flat``) is what an autograd
+    model would hold as ``.grad``; after ``step()`` they contain the
+    rank-ordered mean of every rank's decoded payloads.
+    """
+
+    def __init__(
+        self,
+        spec: CompressorSpec,
+        profile: ModelProfile,
+        partition: Union[Partition, str, None] = None,
+        root_seed: int = 0,
+        group=None,
+        device: Optional[torch.device] = None,
+        stream: Optional[torch.cuda.Stream] = None,
+    ):
+        if not torch.cuda.is_available():
+            raise _native.NativeError("GradSync needs a CUDA device (no CPU fallback)")
+        _native.lib()
+        self.spec = spec
+        self.cspec = spec.to_c()
+        self.profile = profile
+        self.pg = group
+        self.rank, self.world = exchange.world(group)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream or torch.cuda.Stream(device=self.device)
+        self.root_seed = int(root_seed)
+        self.offsets = profile.offsets()
+        self.flat = torch.zeros(self.offsets[-1], dtype=torch.float32, device=self.device)
+        self.grads = [self.flat[a:b] for a, b in zip(self.offsets[:-1], self.offsets[1:])]
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.iteration = 0
+        self._plans: dict[tuple, list[_Group]] = {}
+        self.partition = self._resolve(partition)
+        self.launches_per_step: Optional[int] = None
+
+    # ------------------------------------------------------------ partitions / state
+    def _resolve(self, partition) -> Partition:
+        n = self.profile.n_tensors
+        if partition is None or partition == "merged_all":
+            return Partition.merged(n)
+        if partition == "layer_wise":
+            return Partition.layer_wise(n)
+        if isinstance(partition, Partition):
+            if partition.n_tensors != n:
+                raise ValueError(f"partition is over {partition.n_tensors} tensors, model has {n}")
+            return partition
+        raise ValueError(f"unknown partition literal {partition!r}")
+
+    def _plan(self, partition: Partition) -> list[_Group]:
+        key = partition.boundaries
+        plan = self._plans.get(key)
+        if plan is not None:
+            return plan
+        plan = []
+        ef = self.spec.uses_error_feedback
+        mom = self.spec.momentum_coef is not None
+        for start, end in partition.element_ranges(self.profile):
+            n = end - start
+            L = _native.layout(self.cspec, n)
+            payload = torch.zeros(L.bytes, dtype=torch.uint8, device=self.device)
+            gather = None
+            if self.world > 1 and self.spec.algorithm != "threshold":
+                gather = torch.empty(self.world * L.bytes, dtype=torch.uint8, device=self.device)
+            plan.append(_Group(
+                start, end, L, payload, gather,
+                torch.zeros(n, dtype=torch.float64, device=self.device) if ef else None,
+                torch.zeros(n, dtype=torch.float32, device=self.device) if mom else None,
+            ))
+        self._plans[key] = plan
+        return plan
+
+    def drop_state(self, partition: Optional[Partition] = None) -> None:
+        """Free the EF/momentum state and buffers of one (or every) partition."""
+        if partition is None:
+            self._plans.clear()
+        else:
+            self._plans.pop(partition.boundaries, None)
+
+    def set_gradients(self, flat: torch.Tensor) -> None:
+        self.flat.copy_(flat, non_blocking=True)
+
+    # ------------------------------------------------------------ the sync step
+    def _sync_group(self, g: int, grp: _Group) -> int:
+        """Enqueue encode -> allgather -> decode_mean for one group; returns kernel launches."""
+        seed = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
+        x = self.flat[grp.start:grp.end]
+        device_encode(self.spec, x, grp.residual, grp.momentum, seed[0] | (seed[1] << 64), out=grp.payload,
+                      err=self.err, stream=self.stream, cspec=self.cspec)
+        if self.spec.algorithm == "threshold":
+            gathered, stride, _ = exchange.allgather_variable(grp.payload, group=self.pg)
+        else:
+            gathered, stride = exchange.allgather_fixed(grp.payload, grp.gather, group=self.pg)
+        device_decode_mean(self.spec, gathered, stride, self.world, grp.n, x, self.err, stream=self.stream,
+                           cspec=self.cspec)
+        return 0
+
+    def step(self, partition: Optional[Partition] = None) -> None:
+        """One synchronisation of every group of ``partition`` (default: the pinned one),
+        enqueued on the side stream after the gradients' producer stream."""
+        part = self.partition if partition is None else self._resolve(partition)
+        plan = self._plan(part)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(self.stream):
+            for g, grp in enumerate(plan):
+                self._sync_group(g, grp)
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        self.iteration += 1
+
+    def check(self) -> None:
+        """Raise the reference's ValueError if any device error flag was set."""
+        flags = int(self.err.item())
+        if flags:
+            self.err.zero_()
+            from .compressors import _raise_flags
+
+            _raise_flags(flags)
+
+    # ------------------------------------------------------------ scheduler handle
+    def tensor_profile(self) -> ModelProfile:
+        """trainer.py:325-333 — sizes in backprop order (compute times unknown)."""
+        return ModelProfile(self.profile.name, tuple(LayerProfile(i, l.size, 0.0) for i, l in enumerate(self.profile.layers)))
+
+    def pin_partition(self, partition) -> None:
+        self.partition = self._resolve(partition)
+
+    def timed_iteration(self, partition: Union[Partition, str, None] = None) -> float:
+        """Device time (ms) of one sync step under ``partition`` — CUDA events on the
+        side stream, max over ranks (trainer.py:397-403 uses wall time)."""
+        part = self.partition if partition is None else self._resolve(partition)
+        self._plan(part)
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        start.record(self.stream)
+        self.step(part)
+        stop.record(self.stream)
+        stop.synchronize()
+        ms = start.elapsed_time(stop)
+        if self.world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=self.device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=self.pg)
+            ms = float(t.item())
+        return ms
