@@ -92,6 +92,7 @@ typedef struct mc_layout {
 
 int mc_abi_version(void);
 const char* mc_last_error(void); /* thread-local message of the last failing call */
+int64_t mc_kernel_launches(void); /* kernels launched by this library since load (statistics) */
 
 int64_t mc_top_k_count(double sparsity, int64_t n);
 int64_t mc_payload_bytes(const mc_spec* spec, int64_t n);               /* canonical, incl. 22-B header */

@@ -5,12 +5,16 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 
 #include "mc_internal.cuh"
 
 namespace mc {
 
 static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -116,6 +120,7 @@ extern "C" {
 
 int mc_abi_version(void) { return MC_ABI_VERSION; }
 const char* mc_last_error(void) { return g_err; }
+int64_t mc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int64_t mc_top_k_count(double sparsity, int64_t n) { return top_k_count(sparsity, n); }
 
@@ -286,7 +291,7 @@ int pack_impl(const float* const* srcs, float* const* dsts, const int64_t* numel
     const int64_t total = a.off[a.count];
     if (total > 0) {
       const unsigned grid = (unsigned)imax(1, imin(cdiv(total, 256), (int64_t)sm_count() * 8));
-      k_pack<<<grid, 256, 0, st>>>(a);
+      note_launch(); k_pack<<<grid, 256, 0, st>>>(a);
       MC_LAUNCH_CHECK();
     }
     base += total;
@@ -367,7 +372,7 @@ int mc_serialize(const mc_spec* s, const void* payload, int64_t n, void* out, in
   *out_len = a.start[4];
   if (out_cap < a.start[4]) { set_error("serialize buffer too small (%lld < %lld)", (long long)out_cap, (long long)a.start[4]); return MC_EINVAL; }
   const unsigned grid = (unsigned)imax(1, imin(cdiv(a.start[4], 256), 4096));
-  k_serialize<<<grid, 256, 0, st>>>(a);
+  note_launch(); k_serialize<<<grid, 256, 0, st>>>(a);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }

@@ -136,10 +136,10 @@ int encode_elementwise(const EncodeArgs& a) {
   const unsigned grid = (unsigned)imin(cdiv(a.n, 256), (int64_t)sm_count() * 8);
   cudaStream_t st = a.ctx.stream;
   if (s->algorithm == MC_IDENTITY) {
-    if (p.r) k_elementwise<MC_IDENTITY, true><<<grid, 256, 0, st>>>(p);
+    note_launch(); if (p.r) k_elementwise<MC_IDENTITY, true><<<grid, 256, 0, st>>>(p);
     else k_elementwise<MC_IDENTITY, false><<<grid, 256, 0, st>>>(p);
   } else {
-    if (p.r) k_elementwise<MC_FP16, true><<<grid, 256, 0, st>>>(p);
+    note_launch(); if (p.r) k_elementwise<MC_FP16, true><<<grid, 256, 0, st>>>(p);
     else k_elementwise<MC_FP16, false><<<grid, 256, 0, st>>>(p);
   }
   MC_LAUNCH_CHECK();
@@ -168,7 +168,7 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
   const unsigned grid = (unsigned)imax(1, imin(cdiv(groups, 256), (int64_t)sm_count() * 16));
   cudaStream_t st = c.stream;
 #define MC_DEC_CASE(A) \
-  case A: k_decode_dense<A><<<grid, 256, 0, st>>>(p); break;
+  case A: note_launch(); k_decode_dense<A><<<grid, 256, 0, st>>>(p); break;
   switch (s->algorithm) {
     MC_DEC_CASE(MC_IDENTITY)
     MC_DEC_CASE(MC_FP16)

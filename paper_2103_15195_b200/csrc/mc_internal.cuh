@@ -33,6 +33,7 @@ int64_t top_k_count(double sparsity, int64_t n);
 int fill_layout(const mc_spec* s, int64_t n, int64_t cap, mc_layout* L);
 int sm_count();
 void set_error(const char* fmt, ...);
+void note_launch();  // counts kernel launches (mc_kernel_launches)
 
 // --------------------------------------------------------------------------------------------
 // Per-call launch context.

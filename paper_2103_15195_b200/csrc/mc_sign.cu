@@ -126,13 +126,13 @@ int encode_sign_global(const EncodeArgs& a) {
   // pass 1 reads the un-advanced momentum and advances it: the EF pass then reads m'.
   const int64_t warps = cdiv(a.n, 32);
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(warps * 32, 256), (int64_t)sm_count() * 8));
-  k_sign_pass1<<<g1, 256, 0, st>>>(p);
+  note_launch(); k_sign_pass1<<<g1, 256, 0, st>>>(p);
   const int64_t nodes = 1ll << p.D;
-  k_sign_nodes<<<(unsigned)cdiv(nodes * 32, 256), 256, 0, st>>>(p);
-  k_sign_combine<<<1, 1024, 0, st>>>(p);
+  note_launch(); k_sign_nodes<<<(unsigned)cdiv(nodes * 32, 256), 256, 0, st>>>(p);
+  note_launch(); k_sign_combine<<<1, 1024, 0, st>>>(p);
   if (p.pro.r) {
     const unsigned g = (unsigned)imax(1, imin(cdiv(a.n, 256), (int64_t)sm_count() * 8));
-    k_sign_ef<<<g, 256, 0, st>>>(p);
+    note_launch(); k_sign_ef<<<g, 256, 0, st>>>(p);
   }
   MC_LAUNCH_CHECK();
   return MC_OK;

@@ -637,15 +637,15 @@ int encode_topk(const EncodeArgs& a) {
   const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (nblk + 1);
   if (cudaMemsetAsync(p.w.hist, 0, zbytes, st) != cudaSuccess) return MC_ECUDA;
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 256), (int64_t)sm_count() * 4));
-  k_topk_pass1<<<g1, 256, 0, st>>>(p);
-  k_topk_select1<<<1, 1024, 0, st>>>(p);
-  k_topk_pass2<<<(unsigned)nblk, TB, 0, st>>>(p);
-  k_topk_select2<<<1, 1024, 0, st>>>(p);
-  k_topk_hist3<<<(unsigned)sm_count(), 256, 0, st>>>(p);
-  k_topk_select3<<<1, 1024, 0, st>>>(p);
+  note_launch(); k_topk_pass1<<<g1, 256, 0, st>>>(p);
+  note_launch(); k_topk_select1<<<1, 1024, 0, st>>>(p);
+  note_launch(); k_topk_pass2<<<(unsigned)nblk, TB, 0, st>>>(p);
+  note_launch(); k_topk_select2<<<1, 1024, 0, st>>>(p);
+  note_launch(); k_topk_hist3<<<(unsigned)sm_count(), 256, 0, st>>>(p);
+  note_launch(); k_topk_select3<<<1, 1024, 0, st>>>(p);
   // reset ticket + status for the final look-back pass (list length <= n)
   if (cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st) != cudaSuccess) return MC_ECUDA;
-  k_topk_final<<<(unsigned)nblk, TB, 0, st>>>(p);
+  note_launch(); k_topk_final<<<(unsigned)nblk, TB, 0, st>>>(p);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
@@ -669,7 +669,7 @@ int encode_threshold(const EncodeArgs& a) {
   const int64_t nblk = cdiv(n, TILE);
   cudaStream_t st = a.ctx.stream;
   if (cudaMemsetAsync(w.ticket, 0, 16 + 8 * (nblk + 1), st) != cudaSuccess) return MC_ECUDA;
-  k_threshold<<<(unsigned)nblk, TB, 0, st>>>(p);
+  note_launch(); k_threshold<<<(unsigned)nblk, TB, 0, st>>>(p);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
@@ -701,20 +701,20 @@ int encode_randk(const EncodeArgs& a) {
   if (cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st) != cudaSuccess) return MC_ECUDA;
   if (cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st) != cudaSuccess) return MC_ECUDA;
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 256), (int64_t)sm_count() * 4));
-  k_sparse_prologue<<<g1, 256, 0, st>>>(p.pro, n, p.err, p.payload, p.hdr);
+  note_launch(); k_sparse_prologue<<<g1, 256, 0, st>>>(p.pro, n, p.err, p.payload, p.hdr);
   if (k == n) {
-    k_bitmap_all<<<(unsigned)imax(1, imin(cdiv(nwords, 256), 1024)), 256, 0, st>>>(p);
+    note_launch(); k_bitmap_all<<<(unsigned)imax(1, imin(cdiv(nwords, 256), 1024)), 256, 0, st>>>(p);
   } else {
-    k_randk_walk<<<1, 32, 0, st>>>(p);
+    note_launch(); k_randk_walk<<<1, 32, 0, st>>>(p);
     if (p.tail_shuffle) {
-      k_randk_tail_shuffle<<<1, 1, 0, st>>>(p);
+      note_launch(); k_randk_tail_shuffle<<<1, 1, 0, st>>>(p);
     } else {
       const unsigned gk = (unsigned)imax(1, imin(cdiv(k, 256), (int64_t)sm_count() * 8));
-      k_randk_insert<<<gk, 256, 0, st>>>(p);
-      k_randk_floyd_mark<<<gk, 256, 0, st>>>(p);
+      note_launch(); k_randk_insert<<<gk, 256, 0, st>>>(p);
+      note_launch(); k_randk_floyd_mark<<<gk, 256, 0, st>>>(p);
     }
   }
-  k_randk_emit<<<(unsigned)cdiv(nwords, TB * 4), TB, 0, st>>>(p);
+  note_launch(); k_randk_emit<<<(unsigned)cdiv(nwords, TB * 4), TB, 0, st>>>(p);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
@@ -740,8 +740,8 @@ int decode_mean_sparse(const mc_spec* s, const mc_layout& L, const uint8_t* base
   p.starts = static_cast<uint32_t*>(scratch);
   const int64_t maxcap = L.cap > 0 ? L.cap : L.n;
   dim3 g1((unsigned)imax(1, imin(cdiv(maxcap + 1, 256), (int64_t)sm_count() * 4)), (unsigned)nranks);
-  k_sparse_starts<<<g1, 256, 0, c.stream>>>(p);
-  k_sparse_tiles<<<(unsigned)p.ntiles, 512, 0, c.stream>>>(p);
+  note_launch(); k_sparse_starts<<<g1, 256, 0, c.stream>>>(p);
+  note_launch(); k_sparse_tiles<<<(unsigned)p.ntiles, 512, 0, c.stream>>>(p);
   cudaFreeAsync(scratch, c.stream);
   MC_LAUNCH_CHECK();
   return MC_OK;

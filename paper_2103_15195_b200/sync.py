@@ -84,7 +84,7 @@ class GradSync:
         self.iteration = 0
         self._plans: dict[tuple, list[_Group]] = {}
         self.partition = self._resolve(partition)
-        self.launches_per_step: Optional[int] = None
+        self.probe = None  # (group index, list) -> CUDA events around that group's encode
 
     # ------------------------------------------------------------ partitions / state
     def _resolve(self, partition) -> Partition:
@@ -137,8 +137,15 @@ class GradSync:
         """Enqueue encode -> allgather -> decode_mean for one group; returns kernel launches."""
         seed = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
         x = self.flat[grp.start:grp.end]
+        probe = self.probe is not None and self.probe[0] == g
+        if probe:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(self.stream)
         device_encode(self.spec, x, grp.residual, grp.momentum, seed[0] | (seed[1] << 64), out=grp.payload,
                       err=self.err, stream=self.stream, cspec=self.cspec)
+        if probe:
+            ev[1].record(self.stream)
+            self.probe[1].append(ev)
         if self.spec.algorithm == "threshold":
             gathered, stride, _ = exchange.allgather_variable(grp.payload, group=self.pg)
         else:
@@ -158,6 +165,19 @@ class GradSync:
                 self._sync_group(g, grp)
         torch.cuda.current_stream(self.device).wait_stream(self.stream)
         self.iteration += 1
+
+    def sync_host(self, host_in: torch.Tensor, host_out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The host-buffer entry point: copy a (pinned) host gradient buffer in, run one
+        sync step, copy the averaged gradients back out — all stream-ordered."""
+        if host_out is None:
+            host_out = torch.empty(self.flat.numel(), dtype=torch.float32, pin_memory=True)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(self.stream):
+            self.flat.copy_(host_in, non_blocking=True)
+        self.step()
+        with torch.cuda.stream(self.stream):
+            host_out.copy_(self.flat, non_blocking=True)
+        return host_out
 
     def check(self) -> None:
         """Raise the reference's ValueError if any device error flag was set."""
