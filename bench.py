@@ -321,7 +321,9 @@ def main():
     n_big = sizes[big]
     ef = 16 if spec.uses_error_feedback else 0
     mom = 8 if spec.momentum_coef is not None else 0
-    alg_bytes = n_big * (4 + ef + mom) + (L.bytes - 32)  # read g, r/w residual, write own payload
+    fused = world == 1 and spec.algorithm in ("efsignsgd", "onebit", "int8", "qsgd", "terngrad")
+    # read g, r/w fp64 residual, write own payload (+ write the averaged gradient when fused at N=1)
+    alg_bytes = n_big * (4 + ef + mom + (4 if fused else 0)) + (L.bytes - 32)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms else None
@@ -389,7 +391,7 @@ def main():
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "k_bucket_fast (encode, largest group)",
+                "kernel": ("k_bucket_pipe (fused encode+decode, N=1)" if fused else "encode kernel") + " of the largest group",
                 "achieved": achieved,
                 "peak": peak,
                 "unit": "GB/s",

@@ -111,6 +111,13 @@ int mc_encode(const mc_spec* spec, const float* grad, int64_t n, double* residua
               uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
               uint32_t* err_flags, void* stream);
 
+/* Single-rank sync (world size 1): encode AND out = aggregate([payload]) = 0 + decode(payload)
+ * in the same pass where the codec allows it (bucketed codecs), else encode then decode.
+ * `out` (f32[n]) may alias `grad` (in-place averaged gradient). */
+int mc_encode_decode(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+                     uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
+                     float* out, uint32_t* err_flags, void* stream);
+
 /* out[i] = (sum_{r=0..nranks-1} decode(payload_r)[i]) / f32(nranks), summed in rank
  * order in fp32 exactly as aggregate().  Payload r lives at payloads + r*stride_bytes. */
 int mc_decode_mean(const mc_spec* spec, const void* payloads, int64_t stride_bytes, int32_t nranks,

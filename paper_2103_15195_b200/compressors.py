@@ -47,7 +47,7 @@ from .spec import (
 __all__ = [
     "ALGORITHMS", "HEADER_BYTES", "CompressorSpec", "ResidualState", "CompressedPayload", "DevicePayload",
     "encode", "decode", "aggregate", "payload_bytes", "serialize", "deserialize", "derive_seed",
-    "top_k_count", "empirical_error_bound", "device_encode", "device_decode_mean",
+    "top_k_count", "empirical_error_bound", "device_encode", "device_encode_decode", "device_decode_mean",
 ]
 
 _HDR_DEV = 32  # sizeof(mc_payload_header)
@@ -228,6 +228,30 @@ def device_encode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[t
         "mc_encode",
     )
     return DevicePayload(spec, n, out, L)
+
+
+def device_encode_decode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],
+                         momentum: Optional[torch.Tensor], seed: int, out: torch.Tensor,
+                         payload: Optional[torch.Tensor] = None, err: Optional[torch.Tensor] = None, stream=None,
+                         cspec=None) -> DevicePayload:
+    """Single-rank sync in one pass where the codec allows it: encode ``grad`` and write
+    ``out = aggregate([payload])`` (``out`` may alias ``grad``)."""
+    n = grad.numel()
+    cs = cspec if cspec is not None else spec.to_c()
+    L = _native.layout(cs, n)
+    if payload is None:
+        payload = torch.empty(L.bytes, dtype=torch.uint8, device=grad.device)
+    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n))
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=grad.device)
+    lo, hi = split_seed(seed)
+    _native.check(
+        _native.lib().mc_encode_decode(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum), lo, hi,
+                                       payload.data_ptr(), ws.data_ptr(), ws.numel(), out.data_ptr(), err.data_ptr(),
+                                       _stream_ptr(stream)),
+        "mc_encode_decode",
+    )
+    return DevicePayload(spec, n, payload, L)
 
 
 def device_decode_mean(spec: CompressorSpec, base: torch.Tensor, stride: int, nranks: int, n: int,

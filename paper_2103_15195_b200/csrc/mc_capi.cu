@@ -189,9 +189,9 @@ int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t 
   return MC_OK;
 }
 
-int mc_encode(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum, uint64_t key_lo,
-              uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
-              void* stream) {
+static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                       uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
+                       uint32_t* err_flags, void* stream, float* out) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
   if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
@@ -218,14 +218,34 @@ int mc_encode(const mc_spec* s, const float* grad, int64_t n, double* residual, 
   a.ctx.stream = static_cast<cudaStream_t>(stream);
   a.ctx.err = err_flags;
   switch (s->algorithm) {
-    case MC_IDENTITY: case MC_FP16: return encode_elementwise(a);
-    case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: return encode_bucketed(a);
-    case MC_SIGNSGD: case MC_SIGNUM: return encode_sign_global(a);
-    case MC_TOPK: case MC_DGC_LITE: return encode_topk(a);
-    case MC_RANDK: return encode_randk(a);
-    case MC_THRESHOLD: return encode_threshold(a);
+    case MC_IDENTITY: case MC_FP16: { const int rc = encode_elementwise(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
+    case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: {
+      const int rc = encode_bucketed(a, out);
+      return (rc == MC_FUSED_UNSUPPORTED && !out) ? MC_OK : rc;
+    }
+    case MC_SIGNSGD: case MC_SIGNUM: { const int rc = encode_sign_global(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
+    case MC_TOPK: case MC_DGC_LITE: { const int rc = encode_topk(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
+    case MC_RANDK: { const int rc = encode_randk(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
+    case MC_THRESHOLD: { const int rc = encode_threshold(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
   }
   return MC_EINVAL;
+}
+
+int mc_encode(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum, uint64_t key_lo,
+              uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+              void* stream) {
+  return encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes, err_flags,
+                     stream, nullptr);
+}
+
+int mc_encode_decode(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                     uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
+                     float* out, uint32_t* err_flags, void* stream) {
+  if (!out) { set_error("null output"); return MC_EINVAL; }
+  const int rc = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
+                             err_flags, stream, out);
+  if (rc != MC_FUSED_UNSUPPORTED) return rc;
+  return mc_decode_mean(s, payload, 0, 1, n, out, err_flags, stream);  // two-pass codecs: decode own payload
 }
 
 int mc_decode_mean(const mc_spec* s, const void* payloads, int64_t stride_bytes, int32_t nranks, int64_t n, float* out,

@@ -257,7 +257,10 @@ int64_t sparse_ws_bytes(const mc_spec* s, int64_t n);
 int64_t signglobal_ws_bytes(const mc_spec* s, int64_t n);
 
 int encode_elementwise(const EncodeArgs& a);   // identity, fp16
-int encode_bucketed(const EncodeArgs& a);      // qsgd, efsignsgd, onebit, terngrad, int8
+// `out` (may be null / alias the gradient): also write the single-rank decoded mean in the
+// same pass; returns MC_FUSED_UNSUPPORTED when the chosen path cannot (caller decodes).
+constexpr int MC_FUSED_UNSUPPORTED = 1;
+int encode_bucketed(const EncodeArgs& a, float* out);  // qsgd, efsignsgd, onebit, terngrad, int8
 int encode_sign_global(const EncodeArgs& a);   // signsgd, signum
 int encode_topk(const EncodeArgs& a);          // topk, dgc_lite
 int encode_randk(const EncodeArgs& a);

@@ -28,7 +28,7 @@ from typing import Optional, Sequence, Union
 import torch
 
 from . import _native, exchange
-from .compressors import device_decode_mean, device_encode, split_seed
+from .compressors import device_decode_mean, device_encode, device_encode_decode
 from .profiles import LayerProfile, ModelProfile, Partition
 from .spec import CompressorSpec
 
@@ -85,6 +85,7 @@ class GradSync:
         self._plans: dict[tuple, list[_Group]] = {}
         self.partition = self._resolve(partition)
         self.probe = None  # (group index, list) -> CUDA events around that group's encode
+        self.fuse_local = True  # world size 1: fused encode + decode (mc_encode_decode)
 
     # ------------------------------------------------------------ partitions / state
     def _resolve(self, partition) -> Partition:
@@ -141,7 +142,16 @@ class GradSync:
         if probe:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(self.stream)
-        device_encode(self.spec, x, grp.residual, grp.momentum, seed[0] | (seed[1] << 64), out=grp.payload,
+        key = seed[0] | (seed[1] << 64)
+        if self.world == 1 and self.fuse_local:
+            # single rank: aggregate([payload]) written by the encode pass itself (in place)
+            device_encode_decode(self.spec, x, grp.residual, grp.momentum, key, x, payload=grp.payload, err=self.err,
+                                 stream=self.stream, cspec=self.cspec)
+            if probe:
+                ev[1].record(self.stream)
+                self.probe[1].append(ev)
+            return 0
+        device_encode(self.spec, x, grp.residual, grp.momentum, key, out=grp.payload,
                       err=self.err, stream=self.stream, cspec=self.cspec)
         if probe:
             ev[1].record(self.stream)
