@@ -63,56 +63,117 @@ struct DP {
   uint32_t n_val, n_bits;
 };
 
-template <int ALGO>
-__device__ __forceinline__ float dec1(const DP& p, const uint8_t* pl, int64_t e) {
+// Decode 8 consecutive elements e0 .. e0+7 (e0 % 8 == 0) of one payload.  SAMEB: the 8
+// elements share one bucket (bucket_size % 8 == 0) — one scale load, one sign byte.
+template <int ALGO, bool SAMEB>
+__device__ __forceinline__ void dec8(const DP& p, const uint8_t* pl, uint32_t e0, int cnt, float (&d)[8]) {
   const float* val = reinterpret_cast<const float*>(pl + p.off_val);
   const uint8_t* bits = pl + p.off_bits;
-  if (ALGO == MC_IDENTITY) return val[e];
-  if (ALGO == MC_FP16) return __half2float(reinterpret_cast<const __half*>(bits)[e]);
-  if (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) return __fmul_rn(sign_bit(bits, e) ? 1.0f : -1.0f, val[0]);
-  const int64_t b = e / p.B;
-  if (ALGO == MC_EFSIGNSGD) return __fmul_rn(sign_bit(bits, e) ? 1.0f : -1.0f, val[b]);
-  if (ALGO == MC_ONEBIT) return sign_bit(bits, e) ? val[2 * b + 1] : val[2 * b];
-  if (ALGO == MC_QSGD) {
-    const uint32_t code = read_code(pl + p.off_codes, e, p.width);
-    return __fmul_rn(__fmul_rn(sign_bit(bits, e) ? 1.0f : -1.0f, val[b]), __fdiv_rn((float)code, p.top));
+  if (ALGO == MC_IDENTITY) {
+    if (cnt == 8) {
+      const float4 a = reinterpret_cast<const float4*>(val + e0)[0], b = reinterpret_cast<const float4*>(val + e0)[1];
+      d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w; d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = q < cnt ? val[e0 + q] : 0.0f;
+    }
+    return;
+  }
+  if (ALGO == MC_FP16) {
+    const __half* h = reinterpret_cast<const __half*>(bits) + e0;
+    if (cnt == 8) {
+      const uint4 v = *reinterpret_cast<const uint4*>(h);
+      const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __half22float2(h2[q]);
+        d[2 * q] = f.x;
+        d[2 * q + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = q < cnt ? __half2float(h[q]) : 0.0f;
+    }
+    return;
   }
   if (ALGO == MC_TERNGRAD) {
-    const uint32_t code = (bits[e >> 2] >> (6 - 2 * (e & 3))) & 3u;
-    return __fmul_rn(__fsub_rn((float)code, 1.0f), val[b]);
+    const uint32_t w = bits[e0 >> 2] << 8 | (cnt > 4 ? bits[(e0 >> 2) + 1] : 0u);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float s = val[SAMEB ? e0 / (uint32_t)p.B : (e0 + q) / (uint32_t)p.B];
+      const uint32_t code = (w >> (14 - 2 * q)) & 3u;
+      d[q] = __fmul_rn(__fsub_rn((float)code, 1.0f), s);  // (code - 1) * s   (:501-504)
+    }
+    return;
   }
-  /* MC_INT8 */ return __fmul_rn((float)(int8_t)bits[e], __fdiv_rn(val[b], 127.0f));
+  if (ALGO == MC_INT8) {
+    uint64_t w = 0;
+    if (cnt == 8) w = *reinterpret_cast<const uint64_t*>(bits + e0);
+    else
+      for (int q = 0; q < cnt; ++q) w |= (uint64_t)bits[e0 + q] << (8 * q);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float s = val[SAMEB ? e0 / (uint32_t)p.B : (e0 + q) / (uint32_t)p.B];
+      d[q] = __fmul_rn((float)(int8_t)(uint8_t)(w >> (8 * q)), __fdiv_rn(s, 127.0f));  // (:513)
+    }
+    return;
+  }
+  // sign family: one byte carries the 8 signs, MSB = e0
+  const uint32_t sb = bits[e0 >> 3];
+  uint64_t codes8 = 0;
+  if (ALGO == MC_QSGD && p.width == 8) {
+    const uint8_t* cp = pl + p.off_codes;
+    if (cnt == 8) codes8 = *reinterpret_cast<const uint64_t*>(cp + e0);
+    else
+      for (int q = 0; q < cnt; ++q) codes8 |= (uint64_t)cp[e0 + q] << (8 * q);
+  }
+  const uint32_t b0 = (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) ? 0u : e0 / (uint32_t)p.B;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t b = SAMEB ? b0 : (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) ? 0u : (e0 + q) / (uint32_t)p.B;
+    const float sgn = ((sb >> (7 - q)) & 1u) ? 1.0f : -1.0f;
+    if (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) d[q] = __fmul_rn(sgn, val[0]);
+    else if (ALGO == MC_EFSIGNSGD) d[q] = __fmul_rn(sgn, val[b]);
+    else if (ALGO == MC_ONEBIT) d[q] = ((sb >> (7 - q)) & 1u) ? val[2 * b + 1] : val[2 * b];
+    else {  // MC_QSGD: (sign * s) * (code / (L-1))   (:470)
+      const uint32_t code = p.width == 8 ? (uint32_t)((codes8 >> (8 * q)) & 0xffu)
+                                         : (q < cnt ? read_code(pl + p.off_codes, e0 + q, p.width) : 0u);
+      d[q] = __fmul_rn(__fmul_rn(sgn, val[b]), __fdiv_rn((float)code, p.top));
+    }
+  }
 }
 
-template <int ALGO>
-__global__ void k_decode_dense(DP p) {
+template <int ALGO, bool SAMEB>
+__global__ void __launch_bounds__(256) k_decode_dense(DP p) {
   if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
     const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(p.base + p.stride * threadIdx.x);
     if (h->algorithm != p.algo || h->original_len != (uint64_t)p.n || h->n_val != p.n_val || h->n_bits != p.n_bits)
       atomicOr(p.err, MC_ERR_HEADER);
   }
   const float fn = (float)p.nranks;
-  const int64_t groups = cdiv(p.n, 8);
-  for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = gi * 8;
+  const uint32_t groups = (uint32_t)cdiv(p.n, 8);
+  const bool vout = ((uintptr_t)p.out % 16) == 0;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += gridDim.x * blockDim.x) {
+    const uint32_t e0 = gi * 8;
+    const int cnt = (int)imin(8, p.n - (int64_t)e0);
     float acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
-    for (int r = 0; r < p.nranks; ++r) {
-      const uint8_t* pl = p.base + p.stride * r;
+    for (int r = 0; r < p.nranks; ++r) {  // rank order 0..n-1, fp32 (compressors.py:529-531)
+      float d[8];
+      dec8<ALGO, SAMEB>(p, p.base + p.stride * r, e0, cnt, d);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (e0 + q < p.n) acc[q] = __fadd_rn(acc[q], dec1<ALGO>(p, pl, e0 + q));
+      for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], d[q]);
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], fn);
-    if (e0 + 7 < p.n && ((uintptr_t)(p.out + e0) % 16) == 0) {
+    if (cnt == 8 && vout) {
       reinterpret_cast<float4*>(p.out + e0)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
       reinterpret_cast<float4*>(p.out + e0)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        if (e0 + q < p.n) p.out[e0 + q] = acc[q];
+        if (q < cnt) p.out[e0 + q] = acc[q];
     }
   }
 }
@@ -167,8 +228,13 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
   const int64_t groups = cdiv(L.n, 8);
   const unsigned grid = (unsigned)imax(1, imin(cdiv(groups, 256), (int64_t)sm_count() * 16));
   cudaStream_t st = c.stream;
-#define MC_DEC_CASE(A) \
-  case A: note_launch(); k_decode_dense<A><<<grid, 256, 0, st>>>(p); break;
+  const bool sameb = p.B % 8 == 0;
+#define MC_DEC_CASE(A)                                              \
+  case A:                                                           \
+    note_launch();                                                  \
+    if (sameb) k_decode_dense<A, true><<<grid, 256, 0, st>>>(p);    \
+    else k_decode_dense<A, false><<<grid, 256, 0, st>>>(p);         \
+    break;
   switch (s->algorithm) {
     MC_DEC_CASE(MC_IDENTITY)
     MC_DEC_CASE(MC_FP16)

@@ -32,6 +32,17 @@ def world(group=None) -> tuple[int, int]:
     return 0, 1
 
 
+def _gather_into(out: torch.Tensor, inp: torch.Tensor, group=None) -> None:
+    """all_gather_into_tensor; CUDA tensors on a gloo group are staged through host
+    memory (lets several ranks share one GPU in tests — NCCL is the production path)."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        host = torch.empty(out.numel(), dtype=out.dtype)
+        dist.all_gather_into_tensor(host, inp.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
 def allgather_fixed(payload: torch.Tensor, out: Optional[torch.Tensor] = None, group=None) -> tuple[torch.Tensor, int]:
     """Gather equal-size uint8 payload buffers; returns (gathered, stride)."""
     _, n = world(group)
@@ -40,7 +51,7 @@ def allgather_fixed(payload: torch.Tensor, out: Optional[torch.Tensor] = None, g
         return payload, stride
     if out is None:
         out = torch.empty(n * stride, dtype=torch.uint8, device=payload.device)
-    dist.all_gather_into_tensor(out, payload, group=group)
+    _gather_into(out, payload, group)
     return out, stride
 
 
@@ -70,7 +81,7 @@ def allgather_variable(payload: torch.Tensor, group=None) -> tuple[torch.Tensor,
     if n == 1:
         return payload, payload.numel(), [int(cnt.item())]
     counts = torch.empty(n, dtype=torch.int64, device=payload.device)
-    dist.all_gather_into_tensor(counts, cnt, group=group)
+    _gather_into(counts, cnt.reshape(1), group)
     counts_h = [int(v) for v in counts.cpu().tolist()]  # host sync: the padded size depends on it
     cap = max(max(counts_h), 1)
     mine = _repack(payload, counts_h[r], cap, None)
