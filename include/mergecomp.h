@@ -118,6 +118,15 @@ int mc_encode_decode(const mc_spec* spec, const float* grad, int64_t n, double* 
                      uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
                      float* out, uint32_t* err_flags, void* stream);
 
+/* Chunked variant for pipelining host<->device copies with compute: encode elements
+ * [begin, begin+count) of an n-element group whose buffers start at grad / residual /
+ * momentum / payload / out (whole-group pointers); begin must be a multiple of the bucket
+ * size and of 32, count a multiple of the bucket size unless the chunk ends the group.
+ * Deterministic codecs only (identity, fp16, efsignsgd, onebit, int8); out nullable. */
+int mc_encode_range(const mc_spec* spec, const float* grad, int64_t n, int64_t begin, int64_t count, double* residual,
+                    float* momentum, uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace,
+                    int64_t workspace_bytes, float* out, uint32_t* err_flags, void* stream);
+
 /* out[i] = (sum_{r=0..nranks-1} decode(payload_r)[i]) / f32(nranks), summed in rank
  * order in fp32 exactly as aggregate().  Payload r lives at payloads + r*stride_bytes. */
 int mc_decode_mean(const mc_spec* spec, const void* payloads, int64_t stride_bytes, int32_t nranks,

@@ -57,6 +57,8 @@ _SIGS = {
                                  ctypes.c_int64, _P, _P]),
     "mc_encode_decode": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, ctypes.c_uint64, ctypes.c_uint64, _P, _P,
                                         ctypes.c_int64, _P, _P, _P]),
+    "mc_encode_range": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P,
+                                       ctypes.c_uint64, ctypes.c_uint64, _P, _P, ctypes.c_int64, _P, _P, _P]),
     "mc_decode_mean": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, _P, _P, _P]),
     "mc_pack": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P, _P]),
     "mc_unpack": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P]),

@@ -191,7 +191,7 @@ int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t 
 
 static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
                        uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
-                       uint32_t* err_flags, void* stream, float* out) {
+                       uint32_t* err_flags, void* stream, float* out, int64_t begin = 0, int64_t count = -1) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
   if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
@@ -217,8 +217,18 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
   a.ws_bytes = workspace_bytes;
   a.ctx.stream = static_cast<cudaStream_t>(stream);
   a.ctx.err = err_flags;
+  a.begin = begin;
+  a.count = count;
+  if (begin != 0 || (count >= 0 && count != n)) {  // chunked: deterministic elementwise / bucketed codecs only
+    const int al = s->algorithm;
+    if (begin < 0 || count < 1 || begin + count > n) { set_error("bad chunk [%lld, +%lld)", (long long)begin, (long long)count); return MC_EINVAL; }
+    if (al != MC_IDENTITY && al != MC_FP16 && al != MC_EFSIGNSGD && al != MC_ONEBIT && al != MC_INT8) {
+      set_error("chunked encode unsupported for algorithm %d", al);
+      return MC_EINVAL;
+    }
+  }
   switch (s->algorithm) {
-    case MC_IDENTITY: case MC_FP16: { const int rc = encode_elementwise(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
+    case MC_IDENTITY: case MC_FP16: return encode_elementwise(a, out);
     case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: {
       const int rc = encode_bucketed(a, out);
       return (rc == MC_FUSED_UNSUPPORTED && !out) ? MC_OK : rc;
@@ -236,6 +246,15 @@ int mc_encode(const mc_spec* s, const float* grad, int64_t n, double* residual, 
               void* stream) {
   return encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes, err_flags,
                      stream, nullptr);
+}
+
+int mc_encode_range(const mc_spec* s, const float* grad, int64_t n, int64_t begin, int64_t count, double* residual,
+                    float* momentum, uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace,
+                    int64_t workspace_bytes, float* out, uint32_t* err_flags, void* stream) {
+  const int rc = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
+                             err_flags, stream, out, begin, count);
+  if (rc == MC_FUSED_UNSUPPORTED) { set_error("fused decode unavailable on this path"); return MC_EINVAL; }
+  return rc;
 }
 
 int mc_encode_decode(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,

@@ -18,11 +18,13 @@ struct EP {
   uint32_t* err;
   uint8_t* payload;
   mc_payload_header hdr;
+  float* out;  // single-rank fused decode (may alias g)
+  int write_hdr;
 };
 
-template <int ALGO, bool EF>
+template <int ALGO, bool EF, bool OUT>
 __global__ void k_elementwise(EP p) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
+  if (p.write_hdr && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   bool bad = false;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += (int64_t)gridDim.x * blockDim.x) {
     const float x = p.g[e];
@@ -43,6 +45,7 @@ __global__ void k_elementwise(EP p) {
       dec = __half2float(h);
     }
     if (EF) p.r[e] = __dsub_rn(c, (double)dec);
+    if (OUT) p.out[e] = __fadd_rn(0.0f, dec);  // aggregate([payload]) = (+0 + d) / 1
   }
   flag(p.err, bad, MC_ERR_NONFINITE);
 }
@@ -180,29 +183,35 @@ __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
 
 }  // namespace
 
-int encode_elementwise(const EncodeArgs& a) {
+int encode_elementwise(const EncodeArgs& a, float* out) {
   const mc_spec* s = a.spec;
+  const int64_t begin = a.begin, count = a.count < 0 ? a.n - a.begin : a.count;
   EP p{};
-  p.g = a.g;
-  p.r = s->error_feedback ? a.r : nullptr;
-  p.n = a.n;
-  p.val = reinterpret_cast<float*>(a.payload + a.L.off_val);
-  p.half = reinterpret_cast<__half*>(a.payload + a.L.off_bits);
+  p.g = a.g + begin;
+  p.r = s->error_feedback ? a.r + begin : nullptr;
+  p.n = count;
+  p.val = reinterpret_cast<float*>(a.payload + a.L.off_val) + begin;
+  p.half = reinterpret_cast<__half*>(a.payload + a.L.off_bits) + begin;
   p.err = a.ctx.err;
   p.payload = a.payload;
+  p.out = out ? out + begin : nullptr;
+  p.write_hdr = begin == 0;
   p.hdr.algorithm = (uint32_t)s->algorithm;
   p.hdr.original_len = (uint64_t)a.n;
   p.hdr.n_val = (uint32_t)a.L.n_val;
   p.hdr.n_bits = (uint32_t)a.L.n_bits;
-  const unsigned grid = (unsigned)imin(cdiv(a.n, 256), (int64_t)sm_count() * 8);
+  const unsigned grid = (unsigned)imax(1, imin(cdiv(count, 256), (int64_t)sm_count() * 8));
   cudaStream_t st = a.ctx.stream;
+  note_launch();
+#define MC_EW(A, EF, OUT) k_elementwise<A, EF, OUT><<<grid, 256, 0, st>>>(p)
   if (s->algorithm == MC_IDENTITY) {
-    note_launch(); if (p.r) k_elementwise<MC_IDENTITY, true><<<grid, 256, 0, st>>>(p);
-    else k_elementwise<MC_IDENTITY, false><<<grid, 256, 0, st>>>(p);
+    if (p.r) { if (out) MC_EW(MC_IDENTITY, true, true); else MC_EW(MC_IDENTITY, true, false); }
+    else { if (out) MC_EW(MC_IDENTITY, false, true); else MC_EW(MC_IDENTITY, false, false); }
   } else {
-    note_launch(); if (p.r) k_elementwise<MC_FP16, true><<<grid, 256, 0, st>>>(p);
-    else k_elementwise<MC_FP16, false><<<grid, 256, 0, st>>>(p);
+    if (p.r) { if (out) MC_EW(MC_FP16, true, true); else MC_EW(MC_FP16, true, false); }
+    else { if (out) MC_EW(MC_FP16, false, true); else MC_EW(MC_FP16, false, false); }
   }
+#undef MC_EW
   MC_LAUNCH_CHECK();
   return MC_OK;
 }

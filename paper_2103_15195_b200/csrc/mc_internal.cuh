@@ -250,13 +250,15 @@ struct EncodeArgs {
   uint8_t* ws;
   int64_t ws_bytes;
   Ctx ctx;
+  int64_t begin = 0;   // chunked encode: process elements [begin, begin + count) of the group
+  int64_t count = -1;  // -1: the whole group
 };
 
 int64_t bucket_ws_bytes(const mc_spec* s, int64_t n);
 int64_t sparse_ws_bytes(const mc_spec* s, int64_t n);
 int64_t signglobal_ws_bytes(const mc_spec* s, int64_t n);
 
-int encode_elementwise(const EncodeArgs& a);   // identity, fp16
+int encode_elementwise(const EncodeArgs& a, float* out);  // identity, fp16
 // `out` (may be null / alias the gradient): also write the single-rank decoded mean in the
 // same pass; returns MC_FUSED_UNSUPPORTED when the chosen path cannot (caller decodes).
 constexpr int MC_FUSED_UNSUPPORTED = 1;

@@ -111,3 +111,28 @@ def test_large_group_against_oracle():
             assert np.array_equal(_bits(h.values), _bits(q.values)), algo
             assert np.array_equal(h.bits, q.bits), algo
             assert np.array_equal(_bits(st_d.residual.cpu().numpy()), _bits(st_o.residual)), algo
+
+
+@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8", "fp16", "identity", "qsgd", "dgc_lite"])
+def test_sync_host_pipelined_equals_device_step(algo):
+    """GradSync.sync_host (chunked H2D / fused encode / D2H pipeline) == device step()."""
+    from paper_2103_15195_b200 import gradsets
+    from paper_2103_15195_b200.profiles import Partition
+    from paper_2103_15195_b200.spec import CompressorSpec
+    from paper_2103_15195_b200.sync import GradSync
+
+    spec = CompressorSpec(algo, sparsity=0.99)
+    prof = gradsets.profile("resnet50_161")
+    part = Partition(prof.n_tensors, (100,))
+    a = GradSync(spec, prof, partition=part, root_seed=1)
+    b = GradSync(spec, prof, partition=part, root_seed=1)
+    for it in range(2):
+        g = torch.from_numpy(gradsets.synthetic_gradients("resnet50_161", it, 0)).pin_memory()
+        out = a.sync_host(g, chunk_elems=1 << 20)
+        b.flat.copy_(g)
+        b.step()
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int32), b.flat.cpu().view(torch.int32)), (algo, it)
+        for ga, gb in zip(a._plan(part), b._plan(part)):
+            if ga.residual is not None:
+                assert torch.equal(ga.residual.view(torch.int64), gb.residual.view(torch.int64))
