@@ -129,6 +129,70 @@ __device__ float warp_pairwise(const Get& get, int64_t L) {
   return vals[0];
 }
 
+// Bounded-depth variant for L <= 128 * 2^D (D <= 4 covers L <= 1024 with <= 9 leaves): the
+// leaves of the numpy tree are enumerated by a compile-time-unrolled recursion (warp
+// uniform), summed 4 at a time by 8-lane groups (all 32 lanes busy), and recombined by
+// the same recursion.  Bitwise identical to warp_pairwise.
+namespace pw {
+template <int D>
+__device__ __forceinline__ void collect(int off, int len, int& cnt, int& my_off, int& my_len) {
+  if (D == 0 || len <= 128) {
+    if ((int)(threadIdx.x & 31) == cnt) { my_off = off; my_len = len; }
+    ++cnt;
+    return;
+  }
+  int m = len / 2;
+  m -= m % 8;
+  collect<(D > 0 ? D - 1 : 0)>(off, m, cnt, my_off, my_len);
+  collect<(D > 0 ? D - 1 : 0)>(off + m, len - m, cnt, my_off, my_len);
+}
+template <int D>
+__device__ __forceinline__ float combine(int len, int& cnt, float leafv) {
+  if (D == 0 || len <= 128) return __shfl_sync(0xffffffffu, leafv, cnt++);
+  int m = len / 2;
+  m -= m % 8;
+  const float a = combine<(D > 0 ? D - 1 : 0)>(m, cnt, leafv);
+  const float b = combine<(D > 0 ? D - 1 : 0)>(len - m, cnt, leafv);
+  return __fadd_rn(a, b);
+}
+}  // namespace pw
+
+template <int D, class Get>
+__device__ __forceinline__ float warp_pairwise_small(const Get& get, int L) {
+  const int lane = threadIdx.x & 31;
+  if (L < 8) {  // single short leaf: sequential from -0.0
+    float s = -0.0f;
+    if (lane == 0)
+      for (int q = 0; q < L; ++q) s = __fadd_rn(s, get(q));
+    return __shfl_sync(FULL, s, 0);
+  }
+  int nleaf = 0, my_off = 0, my_len = 0;
+  pw::collect<D>(0, L, nleaf, my_off, my_len);
+  float leafv = 0.0f;  // lane k ends up holding leaf k's sum
+  for (int base = 0; base < nleaf; base += 4) {
+    const int g = lane >> 3, j = lane & 7, leaf = base + g;
+    const int off = __shfl_sync(FULL, my_off, leaf & 31), len = __shfl_sync(FULL, my_len, leaf & 31);
+    const bool act = leaf < nleaf;
+    const int body = act ? len - (len % 8) : 0;
+    float r = act ? get(off + j) : 0.0f;
+#pragma unroll
+    for (int t = 1; t < 16; ++t)
+      if (8 * t < body) r = __fadd_rn(r, get(off + 8 * t + j));
+    r = __fadd_rn(r, __shfl_xor_sync(FULL, r, 1));
+    r = __fadd_rn(r, __shfl_xor_sync(FULL, r, 2));
+    r = __fadd_rn(r, __shfl_xor_sync(FULL, r, 4));
+    if (act && j == 0)
+      for (int q = body; q < len; ++q) r = __fadd_rn(r, get(off + q));
+#pragma unroll
+    for (int gg = 0; gg < 4; ++gg) {
+      const float v = __shfl_sync(FULL, r, 8 * gg);
+      if (lane == base + gg) leafv = v;
+    }
+  }
+  int cnt = 0;
+  return pw::combine<D>(L, cnt, leafv);
+}
+
 // numpy float32 mean of a sequence with a known pairwise sum:  f32( f64(0 + P) / n ).
 __device__ __forceinline__ float np_mean(float pairwise_sum, int64_t n) {
   const float s = __fadd_rn(0.0f, pairwise_sum);
