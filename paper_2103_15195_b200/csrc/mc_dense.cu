@@ -20,32 +20,72 @@ struct EP {
   mc_payload_header hdr;
   float* out;  // single-rank fused decode (may alias g)
   int write_hdr;
+  int vec;  // all streams 16-byte aligned (8 for the fp16 payload): 4-wide vector path
 };
 
 template <int ALGO, bool EF, bool OUT>
 __global__ void k_elementwise(EP p) {
   if (p.write_hdr && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   bool bad = false;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += (int64_t)gridDim.x * blockDim.x) {
-    const float x = p.g[e];
-    bad |= !isfinite(x);
-    double c = (double)x;
-    float c32 = x;
-    if (EF) {
-      c = __dadd_rn((double)x, p.r[e]);
-      c32 = __double2float_rn(c);
-    }
-    float dec;
-    if (ALGO == MC_IDENTITY) {
-      p.val[e] = c32;
-      dec = c32;
+  const int64_t groups = cdiv(p.n, 4);
+  for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = 4 * gi;
+    const bool full = p.vec && e0 + 3 < p.n;
+    float x[4];
+    double rv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (full) {
+      const float4 v = *reinterpret_cast<const float4*>(p.g + e0);
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+      if (EF) {
+        const double2 a = *reinterpret_cast<const double2*>(p.r + e0), b = *reinterpret_cast<const double2*>(p.r + e0 + 2);
+        rv[0] = a.x; rv[1] = a.y; rv[2] = b.x; rv[3] = b.y;
+      }
     } else {
-      const __half h = __float2half_rn(c32);  // numpy astype(float16): RNE, overflow -> inf
-      p.half[e] = h;
-      dec = __half2float(h);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        x[q] = e0 + q < p.n ? p.g[e0 + q] : 0.0f;
+        if (EF) rv[q] = e0 + q < p.n ? p.r[e0 + q] : 0.0;
+      }
     }
-    if (EF) p.r[e] = __dsub_rn(c, (double)dec);
-    if (OUT) p.out[e] = __fadd_rn(0.0f, dec);  // aggregate([payload]) = (+0 + d) / 1
+    float dec[4], c32[4];
+    double c[4];
+    __half h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      bad |= (e0 + q < p.n) && !isfinite(x[q]);
+      c[q] = EF ? __dadd_rn((double)x[q], rv[q]) : (double)x[q];
+      c32[q] = EF ? __double2float_rn(c[q]) : x[q];
+      if (ALGO == MC_IDENTITY) {
+        dec[q] = c32[q];
+      } else {
+        h[q] = __float2half_rn(c32[q]);  // numpy astype(float16): RNE, overflow -> inf
+        dec[q] = __half2float(h[q]);
+      }
+    }
+    if (full) {
+      if (ALGO == MC_IDENTITY) *reinterpret_cast<float4*>(p.val + e0) = make_float4(c32[0], c32[1], c32[2], c32[3]);
+      else {
+        __half2 hv[2] = {__halves2half2(h[0], h[1]), __halves2half2(h[2], h[3])};
+        *reinterpret_cast<uint2*>(p.half + e0) = *reinterpret_cast<uint2*>(hv);
+      }
+      if (EF) {
+        *reinterpret_cast<double2*>(p.r + e0) = make_double2(__dsub_rn(c[0], (double)dec[0]), __dsub_rn(c[1], (double)dec[1]));
+        *reinterpret_cast<double2*>(p.r + e0 + 2) = make_double2(__dsub_rn(c[2], (double)dec[2]), __dsub_rn(c[3], (double)dec[3]));
+      }
+      if (OUT)  // aggregate([payload]) = (+0 + d) / 1
+        *reinterpret_cast<float4*>(p.out + e0) = make_float4(__fadd_rn(0.0f, dec[0]), __fadd_rn(0.0f, dec[1]),
+                                                             __fadd_rn(0.0f, dec[2]), __fadd_rn(0.0f, dec[3]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t e = e0 + q;
+        if (e >= p.n) break;
+        if (ALGO == MC_IDENTITY) p.val[e] = c32[q];
+        else p.half[e] = h[q];
+        if (EF) p.r[e] = __dsub_rn(c[q], (double)dec[q]);
+        if (OUT) p.out[e] = __fadd_rn(0.0f, dec[q]);
+      }
+    }
   }
   flag(p.err, bad, MC_ERR_NONFINITE);
 }
@@ -196,11 +236,13 @@ int encode_elementwise(const EncodeArgs& a, float* out) {
   p.payload = a.payload;
   p.out = out ? out + begin : nullptr;
   p.write_hdr = begin == 0;
+  p.vec = ((uintptr_t)p.g % 16 == 0) && (!p.r || (uintptr_t)p.r % 16 == 0) && ((uintptr_t)p.val % 16 == 0) &&
+          ((uintptr_t)p.half % 8 == 0) && (!p.out || (uintptr_t)p.out % 16 == 0);
   p.hdr.algorithm = (uint32_t)s->algorithm;
   p.hdr.original_len = (uint64_t)a.n;
   p.hdr.n_val = (uint32_t)a.L.n_val;
   p.hdr.n_bits = (uint32_t)a.L.n_bits;
-  const unsigned grid = (unsigned)imax(1, imin(cdiv(count, 256), (int64_t)sm_count() * 8));
+  const unsigned grid = (unsigned)imax(1, imin(cdiv(count, 1024), (int64_t)sm_count() * 16));
   cudaStream_t st = a.ctx.stream;
   note_launch();
 #define MC_EW(A, EF, OUT) k_elementwise<A, EF, OUT><<<grid, 256, 0, st>>>(p)
