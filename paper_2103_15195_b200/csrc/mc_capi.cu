@@ -234,9 +234,12 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
       return (rc == MC_FUSED_UNSUPPORTED && !out) ? MC_OK : rc;
     }
     case MC_SIGNSGD: case MC_SIGNUM: { const int rc = encode_sign_global(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
-    case MC_TOPK: case MC_DGC_LITE: { const int rc = encode_topk(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
-    case MC_RANDK: { const int rc = encode_randk(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
-    case MC_THRESHOLD: { const int rc = encode_threshold(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
+    case MC_TOPK: case MC_DGC_LITE: {
+      if (begin != 0 || (count >= 0 && count != n)) return MC_EINVAL;
+      return encode_topk(a, out);
+    }
+    case MC_RANDK: return encode_randk(a, out);
+    case MC_THRESHOLD: return encode_threshold(a, out);
   }
   return MC_EINVAL;
 }

@@ -221,22 +221,46 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t bid,
   }
   if (lane == 0) { st_volatile(&status[bid], LB_AGG | agg); }
   __threadfence();
+  // Each step inspects a window of 32 lanes x 4 predecessors (newest first), so a block
+  // that has to walk back over many aggregate-only entries (thousands of CTAs in flight)
+  // pays few dependent L2 round trips.
   uint64_t prefix = 0;
   int64_t j = bid - 1;
   while (true) {
-    const int64_t idx = j - lane;
-    uint64_t s = LB_PRE;  // lanes past block 0 behave as an (empty) inclusive prefix
-    if (idx >= 0) {
-      do { s = ld_volatile(&status[idx]); } while ((s >> 62) == 0);
+    uint64_t s[4];
+    // issue the 4 loads back to back (one round trip), then re-poll only unpublished ones
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t idx = j - 4 * lane - q;
+      s[q] = idx >= 0 ? ld_volatile(&status[idx]) : LB_PRE;  // before block 0: empty prefix
     }
-    const unsigned pre = __ballot_sync(FULL, (s >> 62) == 2);
-    const int first = pre ? __ffs(pre) - 1 : 32;  // nearest inclusive prefix
-    uint64_t v = (lane <= first && idx >= 0) ? (s & LB_MASK) : 0;
+    while (true) {
+      bool ready = true;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ready &= (s[q] >> 62) != 0;
+      if (ready) break;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((s[q] >> 62) == 0) s[q] = ld_volatile(&status[j - 4 * lane - q]);
+    }
+    int mine_pre = 4;  // first of my 4 entries (newest first) holding an inclusive prefix
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (mine_pre == 4 && (s[q] >> 62) == 2) mine_pre = q;
+    const unsigned pre = __ballot_sync(FULL, mine_pre < 4);
+    const int first = pre ? __ffs(pre) - 1 : 32;  // lane holding the nearest inclusive prefix
+    uint64_t v = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t idx = j - 4 * lane - q;
+      const bool take = idx >= 0 && (lane < first || (lane == first && q <= mine_pre));
+      v += take ? (s[q] & LB_MASK) : 0;
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     prefix += v;
     if (pre) break;
-    j -= 32;
+    j -= 128;
   }
   if (lane == 0) { st_volatile(&status[bid], LB_PRE | (prefix + agg)); }
   return prefix;
@@ -328,9 +352,9 @@ int encode_elementwise(const EncodeArgs& a, float* out);  // identity, fp16
 constexpr int MC_FUSED_UNSUPPORTED = 1;
 int encode_bucketed(const EncodeArgs& a, float* out);  // qsgd, efsignsgd, onebit, terngrad, int8
 int encode_sign_global(const EncodeArgs& a);   // signsgd, signum
-int encode_topk(const EncodeArgs& a);          // topk, dgc_lite
-int encode_randk(const EncodeArgs& a);
-int encode_threshold(const EncodeArgs& a);
+int encode_topk(const EncodeArgs& a, float* out);  // topk, dgc_lite (out: fused single-rank decode)
+int encode_randk(const EncodeArgs& a, float* out);
+int encode_threshold(const EncodeArgs& a, float* out);
 
 int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks,
                       float* out, const Ctx& c);

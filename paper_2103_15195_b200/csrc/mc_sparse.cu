@@ -38,7 +38,7 @@ int64_t hash_size(int64_t k) {
 
 SparseWS carve(uint8_t* w, int64_t n, int64_t k) {
   SparseWS s{};
-  const int64_t nblk = cdiv(n, TILE) + 1;
+  const int64_t nblk = cdiv(n, 1024) + 1;  // finest look-back tiling in use (k_topk_final)
   s.keys = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
   s.list = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
   s.hist = reinterpret_cast<uint32_t*>(w); w += a16(4 * (2048 + 2048 + 512));
@@ -100,6 +100,19 @@ __device__ __forceinline__ uint64_t block_lookback(uint64_t* status, int64_t bid
 }
 
 // ------------------------------------------------------------------ top-k
+// Radix select over the 31-bit magnitude key of c32 (|x| bits are monotone as u32):
+//   pass1   EF prologue (r <- c in place), keys, 11-bit histogram; (fused N=1) out <- 0
+//   select  bin B1 holding the k-th largest (one CTA)
+//   pass2   ordered compaction (look-back) of every element with bin >= B1 into a list,
+//           histogram of the next 11 bits of the bin-B1 candidates
+//   select2 / hist3 / select3   resolve the exact threshold key T and the tie count
+//   final   ordered filter of the list (key > T, or the first `need` ties = lowest
+//           indices), EF fix-up r = c - c32 on the k survivors, (fused N=1) out[e] = c32
+// Compaction kernels work on warp chunks of 1024 elements (lane holds 128 i + 4 lane + q,
+// i < 8) so loads are coalesced 16-byte vectors; 8 warps = 8192 elements per tile.
+constexpr int CW = 1024;
+constexpr int CB = 8 * CW;
+
 struct TP {
   Prologue pro;
   int64_t n, k;
@@ -107,24 +120,79 @@ struct TP {
   uint32_t* err;
   uint32_t* idx_out;
   float* val_out;
+  float* out;  // fused single-rank decode target (may alias g) or null
+  int vec;
   uint8_t* payload;
   mc_payload_header hdr;
 };
 
-// pass 1: prologue (momentum, EF: r <- c in place), keys, 11-bit histogram of |c32|
 __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
   __shared__ uint32_t h[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) h[i] = 0;
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   bool bad = false;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += (int64_t)gridDim.x * blockDim.x) {
-    float c32;
-    const double c = p.pro.load(e, c32, bad, true);
-    if (p.pro.r) p.pro.r[e] = c;  // residual of unselected elements = c (compressors.py:412)
-    const uint32_t bits = __float_as_uint(c32);
-    p.w.keys[e] = bits;
-    atomicAdd(&h[(bits & 0x7fffffffu) >> 20], 1u);
+  const int64_t groups = cdiv(p.n, 4);
+  for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = 4 * gi;
+    const bool full = p.vec && e0 + 3 < p.n;
+    float x[4] = {0.0f, 0.0f, 0.0f, 0.0f}, mo[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    double rv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (full) {
+      const float4 v = *reinterpret_cast<const float4*>(p.pro.g + e0);
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+      if (p.pro.m) {
+        const float4 m = *reinterpret_cast<const float4*>(p.pro.m + e0);
+        mo[0] = m.x; mo[1] = m.y; mo[2] = m.z; mo[3] = m.w;
+      }
+      if (p.pro.r) {
+        const double2 a = *reinterpret_cast<const double2*>(p.pro.r + e0), b = *reinterpret_cast<const double2*>(p.pro.r + e0 + 2);
+        rv[0] = a.x; rv[1] = a.y; rv[2] = b.x; rv[3] = b.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e0 + q < p.n) {
+          x[q] = p.pro.g[e0 + q];
+          if (p.pro.m) mo[q] = p.pro.m[e0 + q];
+          if (p.pro.r) rv[q] = p.pro.r[e0 + q];
+        }
+    }
+    uint32_t key[4];
+    double c[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool in = e0 + q < p.n;
+      bad |= in && !isfinite(x[q]);
+      float w = x[q];
+      if (p.pro.m) {  // dgc accumulator b*m + x (two roundings, no FMA)  (compressors.py:405)
+        w = p.pro.signum ? __fadd_rn(__fmul_rn(p.pro.beta, mo[q]), __fmul_rn(p.pro.omb, x[q]))
+                         : __fadd_rn(__fmul_rn(p.pro.beta, mo[q]), x[q]);
+        mo[q] = w;
+      }
+      c[q] = p.pro.r ? __dadd_rn((double)w, rv[q]) : (double)w;
+      const float c32 = p.pro.r ? __double2float_rn(c[q]) : w;
+      key[q] = __float_as_uint(c32);
+      if (in) atomicAdd(&h[(key[q] & 0x7fffffffu) >> 20], 1u);
+    }
+    if (full) {
+      *reinterpret_cast<uint4*>(p.w.keys + e0) = make_uint4(key[0], key[1], key[2], key[3]);
+      if (p.pro.m) *reinterpret_cast<float4*>(p.pro.m + e0) = make_float4(mo[0], mo[1], mo[2], mo[3]);
+      if (p.pro.r) {  // residual of unselected elements = c  (compressors.py:412)
+        *reinterpret_cast<double2*>(p.pro.r + e0) = make_double2(c[0], c[1]);
+        *reinterpret_cast<double2*>(p.pro.r + e0 + 2) = make_double2(c[2], c[3]);
+      }
+      if (p.out) *reinterpret_cast<float4*>(p.out + e0) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e0 + q < p.n) {
+          p.w.keys[e0 + q] = key[q];
+          if (p.pro.m) p.pro.m[e0 + q] = mo[q];
+          if (p.pro.r) p.pro.r[e0 + q] = c[q];
+          if (p.out) p.out[e0 + q] = 0.0f;
+        }
+    }
   }
   flag(p.err, bad, MC_ERR_NONFINITE);
   __syncthreads();
@@ -132,13 +200,11 @@ __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
     if (h[i]) atomicAdd(&p.w.hist[i], h[i]);
 }
 
-// find the bin holding the k-th largest: scans nb bins from the top (one block of 1024)
+// find the bin holding the k-th largest: scans nb bins from the top (one CTA of 1024)
 __device__ void select_bin(const uint32_t* hist, int nb, uint32_t k, uint32_t* out_bin, uint32_t* out_krem) {
   __shared__ uint32_t s_w[32];
-  // suffix sums: s_suf[i] = sum hist[i..nb)
   const int per = (nb + blockDim.x - 1) / blockDim.x;  // contiguous bins per thread, descending order
   const int t = threadIdx.x;
-  // thread t owns bins [nb - (t+1)*per, nb - t*per)
   uint32_t own = 0;
   for (int q = 0; q < per; ++q) {
     const int b = nb - t * per - 1 - q;
@@ -161,7 +227,7 @@ __device__ void select_bin(const uint32_t* hist, int nb, uint32_t k, uint32_t* o
     s_w[lane] = wi - w;
   }
   __syncthreads();
-  uint32_t run = s_w[warp] + incl - own;  // count of bins above my range
+  uint32_t run = s_w[warp] + incl - own;  // count in bins above my range
   for (int q = 0; q < per; ++q) {
     const int b = nb - t * per - 1 - q;
     if (b < 0) break;
@@ -175,33 +241,98 @@ __global__ void k_topk_select1(TP p) {
   select_bin(p.w.hist, 2048, (uint32_t)p.k, &p.w.ctl[CTL_B1], &p.w.ctl[CTL_KREM1]);
 }
 
-// pass 2: ordered compaction of every element with bin1 >= B1 into the list; histogram
-// of the next 11 key bits for the elements in bin B1.
-__global__ void __launch_bounds__(TB) k_topk_pass2(TP p) {
+// Warp-chunk ordered compaction helper: given this lane's keep bits (bit 4 i + q for
+// element 128 i + 4 lane + q of the warp chunk), returns this lane's base position for
+// each i (within the warp chunk) and the warp total.
+__device__ __forceinline__ uint32_t warp_chunk_offsets(uint32_t keep, uint32_t (&base)[8]) {
+  const int lane = threadIdx.x & 31;
+  uint32_t run = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t cnt = __popc((keep >> (4 * i)) & 0xfu);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    base[i] = run + incl - cnt;
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  return run;
+}
+
+// CTA-level: exclusive prefix of the 8 warp totals + look-back over tiles.
+__device__ __forceinline__ uint64_t cta_chunk_prefix(uint64_t warp_total, uint64_t* status, int64_t bid,
+                                                     uint64_t& tile_total) {
+  __shared__ uint64_t s_t[8];
+  __shared__ uint64_t s_pre;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_t[warp] = warp_total;
+  __syncthreads();
+  uint64_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    before += (w < warp) ? s_t[w] : 0;
+    tot += s_t[w];
+  }
+  if (warp == 0) {
+    const uint64_t pre = lookback_warp(status, bid, tot);
+    if (lane == 0) s_pre = pre;
+  }
+  __syncthreads();
+  tile_total = tot;
+  const uint64_t r = s_pre + before;
+  __syncthreads();  // s_t / s_pre reused by the next tile
+  return r;
+}
+
+// Persistent: each CTA claims tiles in ticket order until none remain, so the look-back
+// frontier stays close behind (a one-shot grid makes a whole wave walk back at once).
+__global__ void __launch_bounds__(256) k_topk_pass2(TP p, int64_t ntiles) {
   __shared__ uint32_t h2[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) h2[i] = 0;
-  const int64_t bid = take_ticket(p.w.ticket);
   const uint32_t B1 = p.w.ctl[CTL_B1];
-  const int64_t e0 = bid * TILE + (int64_t)threadIdx.x * ITEMS;
-  uint32_t keep = 0;  // bitmask over my ITEMS
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  while (true) {
+    const int64_t bid = take_ticket(p.w.ticket);
+    if (bid >= ntiles) break;
+    const int64_t c0 = bid * CB + (int64_t)warp * CW;
+    uint32_t keep = 0;
+    uint32_t kk[8][4];
 #pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    const int64_t e = e0 + q;
-    if (e < p.n) {
-      const uint32_t key = p.w.keys[e] & 0x7fffffffu;
-      const uint32_t b1 = key >> 20;
-      if (b1 >= B1) keep |= 1u << q;
-      if (b1 == B1) atomicAdd(&h2[(key >> 9) & 0x7ffu], 1u);
+    for (int i = 0; i < 8; ++i) {
+      const int64_t e0 = c0 + 128 * i + 4 * lane;
+      if (e0 + 3 < p.n) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p.w.keys + e0);
+        kk[i][0] = v.x; kk[i][1] = v.y; kk[i][2] = v.z; kk[i][3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kk[i][q] = (e0 + q < p.n) ? p.w.keys[e0 + q] : 0u;
+      }
     }
-  }
-  uint64_t total;
-  const uint64_t ex = block_exscan(__popc(keep), &total);
-  const uint64_t pre = block_lookback(p.w.status, bid, total);
-  uint64_t pos = pre + ex;
 #pragma unroll
-  for (int q = 0; q < ITEMS; ++q)
-    if (keep & (1u << q)) p.w.list[pos++] = (uint32_t)(e0 + q);
-  if (bid == (int64_t)gridDim.x - 1 && threadIdx.x == 0) p.w.ctl[CTL_M] = (uint32_t)(pre + total);
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (c0 + 128 * i + 4 * lane + q >= p.n) continue;
+        const uint32_t key = kk[i][q] & 0x7fffffffu, b1 = key >> 20;
+        if (b1 >= B1) keep |= 1u << (4 * i + q);
+        if (b1 == B1) atomicAdd(&h2[(key >> 9) & 0x7ffu], 1u);
+      }
+    uint32_t base[8];
+    const uint32_t wtot = warp_chunk_offsets(keep, base);
+    uint64_t tile_total;
+    const uint64_t pos0 = cta_chunk_prefix(wtot, p.w.status, bid, tile_total);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t pos = (uint32_t)(pos0 + base[i]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (keep & (1u << (4 * i + q))) p.w.list[pos++] = (uint32_t)(c0 + 128 * i + 4 * lane + q);
+    }
+    if (bid == ntiles - 1 && threadIdx.x == 0) p.w.ctl[CTL_M] = (uint32_t)(pos0 + tile_total);  // list length
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < 2048; i += blockDim.x)
     if (h2[i]) atomicAdd(&p.w.hist[2048 + i], h2[i]);
@@ -237,42 +368,73 @@ __global__ void k_topk_select3(TP p) {
   }
 }
 
-// final: ordered filter of the list: key > T, or key == T among the first `need` ties.
-// Aggregate per block = (gt, ties) packed as 31|31 bits.
-__global__ void __launch_bounds__(TB) k_topk_final(TP p) {
-  const int64_t bid = take_ticket(p.w.ticket);
+// final: persistent, ticketed tiles over the list; per element gt = key > T, tie = key == T.
+// The packed (gt << 32 | tie) prefix gives slot = gt_before + min(tie_before, need).
+// The list is short (k plus one histogram bin), so tiles are small (FI = 1: 1024 entries
+// per CTA) to spread the random key reads over many SMs.
+constexpr int FI = 1;
+constexpr int CB_F = 8 * 128 * FI;
+
+__global__ void __launch_bounds__(256) k_topk_final(TP p) {
   const uint32_t M = p.w.ctl[CTL_M], T = p.w.ctl[CTL_T], need = p.w.ctl[CTL_NEED];
-  if (bid * TILE >= (int64_t)M) return;  // no later block depends on an empty tail block
-  const int64_t i0 = bid * TILE + (int64_t)threadIdx.x * ITEMS;
-  uint32_t gt = 0, tie = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  while (true) {
+    const int64_t bid = take_ticket(p.w.ticket);
+    if (bid * CB_F >= (int64_t)M) break;  // no later tile depends on an empty one
+    const int64_t c0 = bid * CB_F + (int64_t)warp * 128 * FI;
+    uint32_t gt = 0, tie = 0, ent[FI][4];
 #pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    const int64_t i = i0 + q;
-    if (i < M) {
-      const uint32_t key = p.w.keys[p.w.list[i]] & 0x7fffffffu;
-      gt |= (uint32_t)(key > T) << q;
-      tie |= (uint32_t)(key == T) << q;
-    }
-  }
-  const uint64_t mine = ((uint64_t)__popc(gt) << 31) | (uint64_t)__popc(tie);
-  uint64_t total;
-  const uint64_t ex = block_exscan(mine, &total);
-  const uint64_t pre = block_lookback(p.w.status, bid, total);
-  const uint64_t before = pre + ex;
-  uint64_t gt_before = before >> 31, tie_before = before & 0x7fffffffull;
+    for (int i = 0; i < FI; ++i)
 #pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    const bool is_gt = gt & (1u << q), is_tie = tie & (1u << q);
-    if (is_gt || (is_tie && tie_before < need)) {
-      const uint64_t slot = gt_before + (tie_before < need ? tie_before : need);
-      const uint32_t e = p.w.list[i0 + q];
-      const float c32 = __uint_as_float(p.w.keys[e]);
-      p.idx_out[slot] = e;
-      p.val_out[slot] = c32;
-      if (p.pro.r) p.pro.r[e] = __dsub_rn(p.pro.r[e], (double)c32);  // r = c - decode  (:412)
+      for (int q = 0; q < 4; ++q) {
+        const int64_t li = c0 + 128 * i + 4 * lane + q;
+        ent[i][q] = 0;
+        if (li < M) {
+          const uint32_t e = p.w.list[li];
+          ent[i][q] = e;
+          const uint32_t key = p.w.keys[e] & 0x7fffffffu;
+          gt |= (uint32_t)(key > T) << (4 * i + q);
+          tie |= (uint32_t)(key == T) << (4 * i + q);
+        }
+      }
+    // per-i warp scans of the packed counts (gt in the high half, ties in the low half)
+    uint32_t base[FI];
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < FI; ++i) {
+      const uint32_t cnt = (__popc((gt >> (4 * i)) & 0xfu) << 16) | __popc((tie >> (4 * i)) & 0xfu);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      base[i] = run + incl - cnt;
+      run += __shfl_sync(FULL, incl, 31);
     }
-    gt_before += is_gt;
-    tie_before += is_tie;
+    const uint64_t wtot = ((uint64_t)(run >> 16) << 32) | (run & 0xffffu);
+    uint64_t tile_total;
+    const uint64_t pre = cta_chunk_prefix(wtot, p.w.status, bid, tile_total);
+#pragma unroll
+    for (int i = 0; i < FI; ++i) {
+      uint64_t gt_b = (pre >> 32) + (base[i] >> 16), tie_b = (pre & 0xffffffffull) + (base[i] & 0xffffu);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t bit = 1u << (4 * i + q);
+        const bool is_gt = gt & bit, is_tie = tie & bit;
+        if (is_gt || (is_tie && tie_b < need)) {
+          const uint64_t slot = gt_b + (tie_b < need ? tie_b : need);
+          const uint32_t e = ent[i][q];
+          const float c32 = __uint_as_float(p.w.keys[e]);
+          p.idx_out[slot] = e;
+          p.val_out[slot] = c32;
+          if (p.pro.r) p.pro.r[e] = __dsub_rn(p.pro.r[e], (double)c32);  // r = c - decode  (:412)
+          if (p.out) p.out[e] = __fadd_rn(0.0f, c32);                    // aggregate([payload])
+        }
+        gt_b += is_gt;
+        tie_b += is_tie;
+      }
+    }
   }
 }
 
@@ -286,45 +448,117 @@ struct ThP {
   uint32_t* err;
   uint32_t* idx_out;
   float* val_out;
+  float* out;  // fused single-rank decode (may alias g) or null
+  int vec;
+  int64_t ntiles;
   uint8_t* payload;
   mc_payload_header hdr;
 };
 
-__global__ void __launch_bounds__(TB) k_threshold(ThP p) {
-  const int64_t bid = take_ticket(p.ticket);
-  const int64_t e0 = bid * TILE + (int64_t)threadIdx.x * ITEMS;
-  float v[ITEMS];
-  uint32_t keep = 0;
-  bool bad = false;
-#pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    const int64_t e = e0 + q;
-    v[q] = 0.0f;
-    if (e < p.n) {
-      float c32;
-      const double c = p.pro.load(e, c32, bad, true);
-      v[q] = c32;
-      const bool sel = fabsf(c32) >= p.tau;  // |x| >= f32(tau)  (compressors.py:288)
-      keep |= (uint32_t)sel << q;
-      if (p.pro.r) p.pro.r[e] = sel ? __dsub_rn(c, (double)c32) : c;
+// One pass: EF prologue, |c32| >= f32(tau) (compressors.py:288), EF residual, and the
+// ordered compaction of (index, value) by warp chunks + decoupled look-back over tiles;
+// (fused N=1) out = sel ? 0 + c32 : 0.
+template <bool EF, bool MOM>
+__global__ void __launch_bounds__(256) k_threshold(ThP p) {
+  while (true) {
+    const int64_t bid = take_ticket(p.ticket);
+    if (bid >= p.ntiles) break;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c0 = bid * CB + (int64_t)warp * CW;
+    uint32_t keep = 0;
+    float v[8][4];
+    bool bad = false;
+    // all loads of the chunk are issued before any store (the output may alias the input)
+    double rv[EF ? 8 : 1][4];
+    float mo[MOM ? 8 : 1][4];
+  #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t e0 = c0 + 128 * i + 4 * lane;
+      if (p.vec && e0 + 3 < p.n) {
+        const float4 g4 = *reinterpret_cast<const float4*>(p.pro.g + e0);
+        v[i][0] = g4.x; v[i][1] = g4.y; v[i][2] = g4.z; v[i][3] = g4.w;
+        if (MOM) {
+          const float4 m4 = *reinterpret_cast<const float4*>(p.pro.m + e0);
+          mo[MOM ? i : 0][0] = m4.x; mo[MOM ? i : 0][1] = m4.y; mo[MOM ? i : 0][2] = m4.z; mo[MOM ? i : 0][3] = m4.w;
+        }
+        if (EF) {
+          const double2 a = *reinterpret_cast<const double2*>(p.pro.r + e0), b = *reinterpret_cast<const double2*>(p.pro.r + e0 + 2);
+          rv[EF ? i : 0][0] = a.x; rv[EF ? i : 0][1] = a.y; rv[EF ? i : 0][2] = b.x; rv[EF ? i : 0][3] = b.y;
+        }
+      } else {
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool in = e0 + q < p.n;
+          v[i][q] = in ? p.pro.g[e0 + q] : 0.0f;
+          if (MOM) mo[MOM ? i : 0][q] = in ? p.pro.m[e0 + q] : 0.0f;
+          if (EF) rv[EF ? i : 0][q] = in ? p.pro.r[e0 + q] : 0.0;
+        }
+      }
     }
-  }
-  flag(p.err, bad, MC_ERR_NONFINITE);
-  uint64_t total;
-  const uint64_t ex = block_exscan(__popc(keep), &total);
-  const uint64_t pre = block_lookback(p.status, bid, total);
-  uint64_t pos = pre + ex;
-#pragma unroll
-  for (int q = 0; q < ITEMS; ++q)
-    if (keep & (1u << q)) {
-      p.idx_out[pos] = (uint32_t)(e0 + q);
-      p.val_out[pos] = v[q];
-      ++pos;
+  #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t e0 = c0 + 128 * i + 4 * lane;
+      const bool full = p.vec && e0 + 3 < p.n;
+      double rn[4];
+      float o[4], mn[4];
+  #pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool in = e0 + q < p.n;
+        const float x = v[i][q];
+        bad |= in && !isfinite(x);
+        float w = x;
+        if (MOM) {
+          const float m0 = mo[MOM ? i : 0][q];
+          w = p.pro.signum ? __fadd_rn(__fmul_rn(p.pro.beta, m0), __fmul_rn(p.pro.omb, x))
+                           : __fadd_rn(__fmul_rn(p.pro.beta, m0), x);
+          mn[q] = w;
+        }
+        const double c = EF ? __dadd_rn((double)w, rv[EF ? i : 0][q]) : (double)w;
+        const float c32 = EF ? __double2float_rn(c) : w;
+        const bool sel = in && fabsf(c32) >= p.tau;
+        keep |= (uint32_t)sel << (4 * i + q);
+        v[i][q] = c32;
+        rn[q] = sel ? __dsub_rn(c, (double)c32) : c;  // r = c - decode (0 where dropped)
+        o[q] = sel ? __fadd_rn(0.0f, c32) : 0.0f;
+      }
+      if (full) {
+        if (MOM) *reinterpret_cast<float4*>(p.pro.m + e0) = make_float4(mn[0], mn[1], mn[2], mn[3]);
+        if (EF) {
+          *reinterpret_cast<double2*>(p.pro.r + e0) = make_double2(rn[0], rn[1]);
+          *reinterpret_cast<double2*>(p.pro.r + e0 + 2) = make_double2(rn[2], rn[3]);
+        }
+        if (p.out) *reinterpret_cast<float4*>(p.out + e0) = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+  #pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e0 + q < p.n) {
+            if (MOM) p.pro.m[e0 + q] = mn[q];
+            if (EF) p.pro.r[e0 + q] = rn[q];
+            if (p.out) p.out[e0 + q] = o[q];
+          }
+      }
     }
-  if (bid == (int64_t)gridDim.x - 1 && threadIdx.x == 0) {
-    mc_payload_header h = p.hdr;
-    h.n_idx = h.n_val = (uint32_t)(pre + total);
-    *reinterpret_cast<mc_payload_header*>(p.payload) = h;
+    flag(p.err, bad, MC_ERR_NONFINITE);
+    uint32_t base[8];
+    const uint32_t wtot = warp_chunk_offsets(keep, base);
+    uint64_t tile_total;
+    const uint64_t pos0 = cta_chunk_prefix(wtot, p.status, bid, tile_total);
+  #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t pos = (uint32_t)(pos0 + base[i]);
+  #pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (keep & (1u << (4 * i + q))) {
+          p.idx_out[pos] = (uint32_t)(c0 + 128 * i + 4 * lane + q);
+          p.val_out[pos] = v[i][q];
+          ++pos;
+        }
+    }
+    if (bid == p.ntiles - 1 && threadIdx.x == 0) {
+      mc_payload_header h = p.hdr;
+      h.n_idx = h.n_val = (uint32_t)(pos0 + tile_total);
+      *reinterpret_cast<mc_payload_header*>(p.payload) = h;
+    }
   }
 }
 
@@ -340,6 +574,7 @@ struct RP {
   uint32_t* idx_out;
   float* val_out;
   float scale;       // f32(n / k) when unbiased
+  float* out;        // fused single-rank decode target (may alias g) or null
   int unbiased;
   int tail_shuffle;  // numpy's tail-shuffle branch (k > n//50 and n > 10000)
   uint8_t* payload;
@@ -353,38 +588,378 @@ __device__ __forceinline__ uint32_t draw32(const Philox& ph, uint64_t pos) {
   return (pos & 1) ? (uint32_t)(x >> 32) : (uint32_t)x;
 }
 
-// One warp walks the draw stream: step s consumes draws until Lemire accepts for
-// range j_s (Floyd: j_s = n-k+s ascending; tail shuffle: j_s = n-1-s descending).
-__global__ void k_randk_walk(RP p) {
-  const int lane = threadIdx.x;
+// Lemire-32 rejection of numpy's bounded draw in [0, j] (random_bounded_uint64 ->
+// buffered_bounded_lemire_uint32):  m = u32 * (j+1); reject iff lo32(m) < (2^32-(j+1)) % (j+1).
+__device__ __forceinline__ bool lemire_reject(uint32_t w, uint64_t excl, uint32_t& val) {
+  const uint64_t m = (uint64_t)w * excl;
+  val = (uint32_t)(m >> 32);
+  const uint32_t left = (uint32_t)m;
+  if (left >= excl) return false;  // fast accept (the common case)
+  return left < (uint32_t)((0x100000000ull - excl) % excl);  // excl may be 2^32 only via n = 2^32
+}
+
+__device__ __forceinline__ uint64_t step_range(const RP& p, int64_t s) {
+  return p.tail_shuffle ? (uint64_t)(p.n - 1 - s) : (uint64_t)(p.n - p.k + s);
+}
+
+// 32-bit draw stream precomputed in parallel (8 words per Philox block).
+__global__ void k_randk_words(RP p, uint32_t* words, int64_t nwords) {
   const Philox ph{p.k0, p.k1};
-  uint64_t s = 0, pos = 0;
-  while (s < (uint64_t)p.k) {
-    const uint64_t my = s + lane;
-    bool rej = false;
-    uint32_t val = 0;
-    if (my < (uint64_t)p.k) {
-      const uint64_t j = p.tail_shuffle ? (uint64_t)(p.n - 1) - my : (uint64_t)(p.n - p.k) + my;
-      if (j == 0) {
-        val = 0;  // random_bounded_uint64(rng=0) returns without drawing
-      } else {
-        const uint64_t excl = j + 1;
-        const uint64_t m = (uint64_t)draw32(ph, pos + lane) * excl;
-        const uint32_t left = (uint32_t)m;
-        if (left < excl) {
-          const uint32_t thr = (uint32_t)((0x100000000ull - excl) % excl);
-          rej = left < thr;
-        }
-        val = (uint32_t)(m >> 32);
+  for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 8 * blk < nwords;
+       blk += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    ph.block(blk, w);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (8 * blk + 2 * q < nwords) words[8 * blk + 2 * q] = (uint32_t)w[q];
+      if (8 * blk + 2 * q + 1 < nwords) words[8 * blk + 2 * q + 1] = (uint32_t)(w[q] >> 32);
+    }
+  }
+}
+
+// One CTA walks the draw stream in windows of 1024 positions.  Step s consumes draws
+// until Lemire accepts for range j_s, so position q serves step q - t(q) with t the
+// rejections before q.  Per window every position evaluates 16 candidate offsets t0+d
+// (warp ballots -> masks), each warp turns its masks into a transition table
+// d_in -> d_out, one thread composes the 32 tables to get every warp's entering offset,
+// and accepted positions emit draws[step].  A window is truncated at the first warp
+// whose offset would leave the 16 candidates (more rejections than candidates).
+constexpr int WD = 16;
+
+__global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words, int64_t nwords,
+                                                     const int64_t* start /* base, t0 or null */) {
+  __shared__ uint32_t smask[32][WD];
+  __shared__ uint8_t sF[32][WD];
+  __shared__ int s_enter[33];
+  __shared__ int s_nw;
+  __shared__ int64_t s_base, s_t0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Philox ph{p.k0, p.k1};
+  if (start && start[0] < 0) return;  // the multi-SM walk served every step
+  if (tid == 0) { s_base = start ? start[0] : 0; s_t0 = start ? start[1] : 0; }
+  __syncthreads();
+  int64_t pf_pos = s_base + tid;  // prefetched word for the (likely) next window position
+  uint32_t pf = pf_pos < nwords ? words[pf_pos] : draw32(ph, (uint64_t)pf_pos);
+  while (true) {
+    const int64_t base = s_base, t0 = s_t0;
+    if (base - t0 >= p.k) break;  // every step has its draw
+    const int64_t pos = base + tid;
+    const uint32_t w32 = pos == pf_pos ? pf : (pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos));
+    pf_pos = pos + 1024;
+    if (pf_pos < nwords) pf = words[pf_pos];
+    else pf = draw32(ph, (uint64_t)pf_pos);
+    // candidate d serves step s = pos - t0 - d with range excl_d = j_s + 1 = A + s (Floyd) or
+    // A - s (tail shuffle).  Since lo32(w * excl_d) = lo32(w * excl_0) -+ d * w, the fast
+    // accept test (left >= excl, i.e. no rejection possible) costs two integer ops per d;
+    // the exact Lemire threshold is evaluated only for the rare candidates that fail it.
+    const int64_t s0 = pos - t0;
+    const uint32_t A = p.tail_shuffle ? (uint32_t)p.n : (uint32_t)(p.n - p.k + 1);
+    const uint32_t ex0 = p.tail_shuffle ? A - (uint32_t)s0 : A + (uint32_t)s0;
+    const uint32_t l0 = w32 * ex0;  // lo32 of the product
+    const uint32_t dl = p.tail_shuffle ? w32 : (0u - w32);  // left_d = l0 + d * dl
+    uint32_t hit = 0;  // bit d: candidate d may reject
+#pragma unroll
+    for (int d = 0; d < WD; ++d) {
+      const uint32_t ex = p.tail_shuffle ? ex0 + d : ex0 - d;
+      hit |= (uint32_t)((l0 + (uint32_t)d * dl) < ex) << d;
+    }
+    if (hit) {  // exact test for the candidates that can reject, with step validity
+      uint32_t rejm = 0;
+      for (uint32_t h = hit; h; h &= h - 1) {
+        const int d = __ffs(h) - 1;
+        const int64_t s = s0 - d;
+        const uint32_t ex = p.tail_shuffle ? ex0 + d : ex0 - d;
+        const uint32_t left = l0 + (uint32_t)d * dl;
+        if (s >= 0 && s < p.k && left < (0u - ex) % ex) rejm |= 1u << d;  // (2^32 - ex) mod ex
+      }
+      hit = rejm;
+    }
+    // transpose: mask for candidate d = lanes whose bit d is set
+#pragma unroll
+    for (int d = 0; d < WD; ++d) {
+      const unsigned mb = __ballot_sync(FULL, (hit >> d) & 1u);
+      if (lane == 0) smask[warp][d] = mb;
+    }
+    __syncthreads();
+    if (lane < WD) {  // transition table of this warp: entering offset d -> leaving offset
+      int d = lane, from = 0;
+      while (from < 32) {
+        const uint32_t m = smask[warp][d] & (0xffffffffu << from);
+        if (!m) break;
+        from = __ffs(m);  // position after the rejection
+        if (++d >= WD) { d = 255; break; }
+      }
+      sF[warp][lane] = (uint8_t)d;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // compose the 32 tables in warp order; identity tables (no rejection for any d, the
+      // common case) leave the offset unchanged, so only the others are walked serially
+      bool ident = true;
+#pragma unroll
+      for (int d = 0; d < WD; ++d) ident &= sF[lane][d] == d;
+      unsigned todo = __ballot_sync(FULL, !ident);
+      int d = 0, nw = 32, enter = 0;
+      while (todo) {
+        const int w = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int nd = sF[w][d];  // uniform smem read
+        if (nd == 255) { nw = w; break; }
+        d = nd;
+        if (lane > w) enter = d;
+      }
+      s_enter[lane] = enter;  // entering offset of warp `lane` (valid for lane <= nw)
+      if (lane == 0) {
+        s_enter[32] = d;
+        s_nw = nw;
       }
     }
-    // j == 0 consumes no draw: only possible for the very first Floyd step with k == n,
-    // which the host routes to the full selection path.
-    const unsigned rm = __ballot_sync(FULL, rej);
-    const int f = rm ? __ffs(rm) - 1 : 32;
-    if (lane < f && my < (uint64_t)p.k) p.w.draws[my] = val;
-    s += f;
-    pos += f + (rm ? 1 : 0);
+    __syncthreads();
+    const int nw = s_nw;
+    if (nw == 0) {
+      // > WD rejections inside one warp's 32 positions: walk them one by one (never seen in practice)
+      if (tid == 0) {
+        int64_t q = base, t = t0;
+        for (int i = 0; i < 32 && q - t < p.k; ++i, ++q) {
+          uint32_t v;
+          const uint32_t w = q < nwords ? words[q] : draw32(ph, (uint64_t)q);
+          if (lemire_reject(w, step_range(p, q - t) + 1, v)) ++t;
+          else p.w.draws[q - t] = v;
+        }
+        s_base = q;
+        s_t0 = t;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (warp < nw) {
+      // rejection positions of this warp along the true path, from its entering offset
+      uint32_t R = 0;
+      if (lane == 0) {
+        int d = s_enter[warp], from = 0;
+        while (from < 32) {
+          const uint32_t m = smask[warp][d] & (0xffffffffu << from);
+          if (!m) break;
+          const int f = __ffs(m) - 1;
+          R |= 1u << f;
+          from = f + 1;
+          ++d;
+        }
+      }
+      R = __shfl_sync(FULL, R, 0);
+      const int d = s_enter[warp] + __popc(R & ((1u << lane) - 1));
+      const int64_t s = pos - t0 - d;
+      if (!((R >> lane) & 1u) && s >= 0 && s < p.k) {
+        uint32_t v;
+        lemire_reject(w32, step_range(p, s) + 1, v);
+        p.w.draws[s] = v;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_base = base + 32 * nw;
+      s_t0 = t0 + s_enter[nw];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- multi-SM draw walk ------------------------------------------------------------------
+// The draw stream is cut into windows of WP = 1024 positions.  The offset t (rejections so
+// far) at a window's start is unknown, but it is close to its expectation E_w (the sum of the
+// per-draw rejection probabilities ((2^32 - excl) mod excl) / 2^32 before the window):
+//   tables  one CTA per window evaluates the window for every entering offset
+//           t in [L_w, L_w + DW) with L_w = E_w - DW/2 (rejection masks for all offsets
+//           in smem, then one thread per candidate walks them) -> rejections r_w(t);
+//   chain   one CTA composes t_{w+1} = t_w + r_w(t_w) (one smem lookup per window);
+//   emit    one CTA per window re-walks from its exact t_w and writes draws[step];
+//   fallback if t_w ever leaves [L_w, L_w + DW) (a > 7 sigma excursion) the single-CTA
+//           walker finishes the stream from that window.
+constexpr int WP = 1024, DW = 512, RX = 32;
+
+struct WalkCtl {
+  int64_t fail_base, fail_t0;  // fallback start (fail_base < 0: none)
+  int64_t nwin_used;
+};
+
+__device__ __forceinline__ uint32_t excl_of(const RP& p, int64_t s) {
+  return p.tail_shuffle ? (uint32_t)(p.n - s) : (uint32_t)(p.n - p.k + 1 + s);
+}
+
+// rejection test of position word w32 for step s (fast accept, then the exact threshold)
+__device__ __forceinline__ bool rejects(const RP& p, uint32_t w32, int64_t s) {
+  if (s < 0 || s >= p.k) return false;
+  const uint32_t ex = excl_of(p, s);
+  const uint32_t left = w32 * ex;
+  return left < ex && left < (0u - ex) % ex;
+}
+
+__global__ void k_randk_expect(RP p, double* expw, int64_t nwin) {
+  __shared__ double part[8];
+  const int64_t w = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < WP; i += blockDim.x) {
+    const int64_t s = imin(imax(w * WP + i, 0), p.k - 1);
+    const uint32_t ex = excl_of(p, s);
+    acc += (double)((0u - ex) % ex) * 0x1.0p-32;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    expw[w] = t;
+  }
+}
+
+__global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, const double* expw, int64_t* Lw,
+                               uint8_t* tables) {
+  extern __shared__ uint32_t masks[];  // [DW + RX][32]
+  __shared__ int64_t s_L;
+  const int64_t w = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    double e = 0.0;  // expected offset at the window start (sum of earlier windows)
+    for (int64_t i = 0; i < w; ++i) e += expw[i];
+    const int64_t L = imax(0, (int64_t)floor(e) - DW / 2);
+    s_L = L;
+    Lw[w] = L;
+  }
+  __syncthreads();
+  const int64_t L = s_L;
+  const Philox ph{p.k0, p.k1};
+  const int64_t pos = w * WP + tid;
+  const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
+  // candidate c serves step s = pos - L - c; lo32(w * excl) moves by -+w per candidate, so the
+  // "may reject" filter (left < excl) is two integer ops; exact thresholds only for hits
+  const int64_t s0 = pos - L;
+  const uint32_t ex0 = excl_of(p, s0);
+  const uint32_t l0 = w32 * ex0;
+  const uint32_t dl = p.tail_shuffle ? w32 : (0u - w32);
+  for (int c0 = 0; c0 < DW + RX; c0 += 32) {
+    uint32_t hit = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t ex = p.tail_shuffle ? ex0 + (uint32_t)(c0 + c) : ex0 - (uint32_t)(c0 + c);
+      hit |= (uint32_t)((l0 + (uint32_t)(c0 + c) * dl) < ex) << c;
+    }
+    for (uint32_t h = hit; h; h &= h - 1) {
+      const int c = __ffs(h) - 1;
+      if (!rejects(p, w32, s0 - (c0 + c))) hit &= ~(1u << c);
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const unsigned m = __ballot_sync(FULL, (hit >> c) & 1u);
+      if (lane == 0) masks[(c0 + c) * 32 + warp] = m;
+    }
+  }
+  __syncthreads();
+  if (tid < DW) {  // walk entering with offset L + tid
+    int d = tid, bit = 0;
+    bool ok = true;
+    while (bit < WP) {
+      const int word = bit >> 5;
+      const uint32_t m = masks[d * 32 + word] & (0xffffffffu << (bit & 31));
+      if (!m) { bit = (word + 1) * 32; continue; }
+      bit = word * 32 + __ffs(m);  // position after the rejection
+      if (++d >= DW + RX || d - tid >= RX) { ok = false; break; }
+    }
+    tables[w * DW + tid] = ok ? (uint8_t)(d - tid) : (uint8_t)255;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, const uint8_t* tables, int64_t nwin,
+                                                      int64_t* tin, WalkCtl* ctl) {
+  extern __shared__ uint8_t srow[];  // [CH][DW]
+  constexpr int CH = 96;
+  __shared__ int64_t s_L[CH];
+  __shared__ int64_t s_t;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) { s_t = 0; s_stop = 0; ctl->fail_base = -1; ctl->nwin_used = nwin; }
+  __syncthreads();
+  for (int64_t w0 = 0; w0 < nwin && !s_stop; w0 += CH) {
+    const int cnt = (int)imin(CH, nwin - w0);
+    const uint4* src = reinterpret_cast<const uint4*>(tables + w0 * DW);
+    for (int i = threadIdx.x; i < cnt * DW / 16; i += blockDim.x) reinterpret_cast<uint4*>(srow)[i] = src[i];
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) s_L[i] = Lw[w0 + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = s_t;
+      for (int i = 0; i < cnt; ++i) {
+        const int64_t w = w0 + i;
+        if (w * WP - t >= p.k) { ctl->nwin_used = w; s_stop = 1; break; }  // every step served
+        const int64_t c = t - s_L[i];
+        const uint8_t r = (c >= 0 && c < DW) ? srow[i * DW + c] : (uint8_t)255;
+        if (r == 255) {  // outside the speculated range: hand over to the serial walker
+          ctl->fail_base = w * WP;
+          ctl->fail_t0 = t;
+          ctl->nwin_used = w;
+          s_stop = 1;
+          break;
+        }
+        tin[w] = t;
+        t += r;
+      }
+      s_t = t;
+      if (!s_stop && w0 + cnt >= nwin && nwin * WP - t < p.k) {  // ran out of windows
+        ctl->fail_base = nwin * WP;
+        ctl->fail_t0 = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_randk_emit_draws(RP p, const uint32_t* words, int64_t nwords,
+                                                           const int64_t* tin, const WalkCtl* ctl) {
+  __shared__ uint32_t smask[RX][32];
+  __shared__ int s_enter[32];
+  const int64_t w = blockIdx.x;
+  if (w >= ctl->nwin_used) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t t0 = tin[w];
+  const Philox ph{p.k0, p.k1};
+  const int64_t pos = w * WP + tid;
+  const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
+  for (int d = 0; d < RX; ++d) {
+    const unsigned m = __ballot_sync(FULL, rejects(p, w32, pos - t0 - d));
+    if (lane == 0) smask[d][warp] = m;
+  }
+  __syncthreads();
+  if (tid == 0) {  // entering offsets of the 32 warps along the true path (<= RX-1 rejections)
+    int d = 0;
+    for (int wi = 0; wi < 32; ++wi) {
+      s_enter[wi] = d;
+      int bit = 0;
+      while (bit < 32) {
+        const uint32_t m = smask[d][wi] & (0xffffffffu << bit);
+        if (!m) break;
+        bit = __ffs(m);
+        ++d;
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t R = 0;  // rejection positions of this warp
+  if (lane == 0) {
+    int d = s_enter[warp], bit = 0;
+    while (bit < 32) {
+      const uint32_t m = smask[d][warp] & (0xffffffffu << bit);
+      if (!m) break;
+      const int f = __ffs(m) - 1;
+      R |= 1u << f;
+      bit = f + 1;
+      ++d;
+    }
+  }
+  R = __shfl_sync(FULL, R, 0);
+  const int d = s_enter[warp] + __popc(R & ((1u << lane) - 1));
+  const int64_t s = pos - t0 - d;
+  if (!((R >> lane) & 1u) && s >= 0 && s < p.k) {
+    uint32_t v;
+    lemire_reject(w32, (uint64_t)excl_of(p, s), v);
+    p.w.draws[s] = v;
   }
 }
 
@@ -482,6 +1057,7 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
   const uint64_t ex = block_exscan(cnt, &total);
   const uint64_t pre = block_lookback(p.w.status, bid, total);
   uint64_t pos = pre + ex;
+  const uint64_t pos_start = pos;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t m = words[q];
@@ -507,10 +1083,43 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
       ++pos;
     }
   }
+  if (p.out) {  // fused single-rank decode of the CTA's 32768 elements: 0 + v where selected, else 0
+    __shared__ uint32_t s_words[TB * 4], s_rank[TB * 4];
+    uint32_t rk = (uint32_t)pos_start;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s_words[threadIdx.x * 4 + q] = words[q];
+      s_rank[threadIdx.x * 4 + q] = rk;
+      rk += __popc(words[q]);
+    }
+    __syncthreads();  // also orders this CTA's val_out writes before the reads below
+    const int64_t e_base = bid * TB * 4 * 32;
+    const bool vec = ((uintptr_t)(p.out + e_base) % 16) == 0;
+    for (int i = threadIdx.x; i < TB * 4 * 8; i += blockDim.x) {  // float4 groups, coalesced
+      const int wi = i >> 3, sh = (i & 7) * 4;
+      const int64_t e = e_base + 4 * (int64_t)i;
+      if (e >= p.n) break;
+      const uint32_t wd = s_words[wi];
+      float v[4];
+      uint32_t r = s_rank[wi] + __popc(wd & ((1u << sh) - 1u));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool sel = (wd >> (sh + q)) & 1u;
+        v[q] = sel ? __fadd_rn(0.0f, p.val_out[r]) : 0.0f;
+        r += sel;
+      }
+      if (vec && e + 3 < p.n) {
+        *reinterpret_cast<float4*>(p.out + e) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+        for (int q = 0; q < 4 && e + q < p.n; ++q) p.out[e + q] = v[q];
+      }
+    }
+  }
 }
 
 // prologue pass for randk (momentum/EF state update, non-finite check; no keys needed)
-__global__ void k_sparse_prologue(Prologue pro, int64_t n, uint32_t* err, uint8_t* payload, mc_payload_header hdr) {
+__global__ void k_sparse_prologue(Prologue pro, int64_t n, uint32_t* err, uint8_t* payload, mc_payload_header hdr,
+                                  float* out) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(payload) = hdr;
   bool bad = false;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -532,7 +1141,7 @@ struct SD {
   uint32_t* err;
   uint32_t algo;
 };
-constexpr int DT = 4096;  // output tile (elements)
+constexpr int DT = 8192;  // output tile (elements, 32 KB of smem)
 
 __device__ __forceinline__ void sparse_sections(const uint8_t* pl, const uint32_t*& idx, const float*& val, uint32_t& cnt) {
   const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(pl);
@@ -571,11 +1180,12 @@ __global__ void k_sparse_starts(SD p) {
   }
 }
 
-__global__ void __launch_bounds__(512) k_sparse_tiles(SD p) {
-  __shared__ float acc[DT];
+__global__ void __launch_bounds__(256) k_sparse_tiles(SD p) {
+  __shared__ __align__(16) float acc[DT];
   const int64_t t = blockIdx.x;
   const int64_t t0 = t * DT;
-  for (int i = threadIdx.x; i < DT; i += blockDim.x) acc[i] = 0.0f;
+  for (int i = threadIdx.x; i < DT / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(acc)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   __syncthreads();
   for (int r = 0; r < p.nranks; ++r) {
     const uint8_t* pl = p.base + p.stride * r;
@@ -593,7 +1203,15 @@ __global__ void __launch_bounds__(512) k_sparse_tiles(SD p) {
   }
   const float fn = (float)p.nranks;
   const int64_t lim = imin(DT, p.n - t0);
-  for (int i = threadIdx.x; i < lim; i += blockDim.x) p.out[t0 + i] = __fdiv_rn(acc[i], fn);
+  if (lim == DT && ((uintptr_t)(p.out + t0) % 16) == 0) {
+    for (int i = threadIdx.x; i < DT / 4; i += blockDim.x) {
+      const float4 v = reinterpret_cast<const float4*>(acc)[i];
+      reinterpret_cast<float4*>(p.out + t0)[i] =
+          make_float4(__fdiv_rn(v.x, fn), __fdiv_rn(v.y, fn), __fdiv_rn(v.z, fn), __fdiv_rn(v.w, fn));
+    }
+  } else {
+    for (int i = threadIdx.x; i < lim; i += blockDim.x) p.out[t0 + i] = __fdiv_rn(acc[i], fn);
+  }
 }
 
 }  // namespace
@@ -617,7 +1235,7 @@ static Prologue make_prologue(const EncodeArgs& a) {
   return pro;
 }
 
-int encode_topk(const EncodeArgs& a) {
+int encode_topk(const EncodeArgs& a, float* out) {
   const int64_t n = a.n, k = top_k_count(a.spec->sparsity, n);
   TP p{};
   p.pro = make_prologue(a);
@@ -627,30 +1245,34 @@ int encode_topk(const EncodeArgs& a) {
   p.err = a.ctx.err;
   p.idx_out = reinterpret_cast<uint32_t*>(a.payload + a.L.off_idx);
   p.val_out = reinterpret_cast<float*>(a.payload + a.L.off_val);
+  p.out = out;
+  p.vec = ((uintptr_t)p.pro.g % 16 == 0) && (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) &&
+          (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0) && ((uintptr_t)out % 16 == 0);
   p.payload = a.payload;
   p.hdr.algorithm = (uint32_t)a.spec->algorithm;
   p.hdr.original_len = (uint64_t)n;
   p.hdr.n_idx = p.hdr.n_val = p.hdr.cap = (uint32_t)k;
   cudaStream_t st = a.ctx.stream;
-  const int64_t nblk = cdiv(n, TILE);
+  const int64_t ntiles = cdiv(n, CB);
   // zero histograms + ctl + ticket + status in one memset (contiguous in the carve)
-  const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (nblk + 1);
+  const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (ntiles + 1);
   if (cudaMemsetAsync(p.w.hist, 0, zbytes, st) != cudaSuccess) return MC_ECUDA;
-  const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 256), (int64_t)sm_count() * 4));
+  const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 1024), (int64_t)sm_count() * 8));
   note_launch(); k_topk_pass1<<<g1, 256, 0, st>>>(p);
   note_launch(); k_topk_select1<<<1, 1024, 0, st>>>(p);
-  note_launch(); k_topk_pass2<<<(unsigned)nblk, TB, 0, st>>>(p);
+  note_launch(); k_topk_pass2<<<(unsigned)imax(1, imin(ntiles, (int64_t)sm_count() * 4)), 256, 0, st>>>(p, ntiles);
   note_launch(); k_topk_select2<<<1, 1024, 0, st>>>(p);
   note_launch(); k_topk_hist3<<<(unsigned)sm_count(), 256, 0, st>>>(p);
   note_launch(); k_topk_select3<<<1, 1024, 0, st>>>(p);
   // reset ticket + status for the final look-back pass (list length <= n)
-  if (cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st) != cudaSuccess) return MC_ECUDA;
-  note_launch(); k_topk_final<<<(unsigned)nblk, TB, 0, st>>>(p);
+  const int64_t ftiles = cdiv(n, CB_F);
+  if (cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (ftiles + 1), st) != cudaSuccess) return MC_ECUDA;
+  note_launch(); k_topk_final<<<(unsigned)imax(1, imin(ftiles, (int64_t)sm_count() * 4)), 256, 0, st>>>(p);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
 
-int encode_threshold(const EncodeArgs& a) {
+int encode_threshold(const EncodeArgs& a, float* out) {
   const int64_t n = a.n;
   ThP p{};
   p.pro = make_prologue(a);
@@ -666,15 +1288,27 @@ int encode_threshold(const EncodeArgs& a) {
   p.hdr.algorithm = MC_THRESHOLD;
   p.hdr.original_len = (uint64_t)n;
   p.hdr.cap = (uint32_t)a.L.cap;
-  const int64_t nblk = cdiv(n, TILE);
+  p.out = out;
+  p.vec = ((uintptr_t)p.pro.g % 16 == 0) && (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) &&
+          (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0) && ((uintptr_t)out % 16 == 0);
+  const int64_t nblk = cdiv(n, CB);
+  p.ntiles = nblk;
   cudaStream_t st = a.ctx.stream;
   if (cudaMemsetAsync(w.ticket, 0, 16 + 8 * (nblk + 1), st) != cudaSuccess) return MC_ECUDA;
-  note_launch(); k_threshold<<<(unsigned)nblk, TB, 0, st>>>(p);
+  const unsigned pgrid = (unsigned)imax(1, imin(nblk, (int64_t)sm_count() * 2));
+  note_launch();
+  if (p.pro.r) {
+    if (p.pro.m) k_threshold<true, true><<<pgrid, 256, 0, st>>>(p);
+    else k_threshold<true, false><<<pgrid, 256, 0, st>>>(p);
+  } else {
+    if (p.pro.m) k_threshold<false, true><<<pgrid, 256, 0, st>>>(p);
+    else k_threshold<false, false><<<pgrid, 256, 0, st>>>(p);
+  }
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
 
-int encode_randk(const EncodeArgs& a) {
+int encode_randk(const EncodeArgs& a, float* out) {
   const int64_t n = a.n, k = top_k_count(a.spec->sparsity, n);
   RP p{};
   p.pro = make_prologue(a);
@@ -689,6 +1323,7 @@ int encode_randk(const EncodeArgs& a) {
   p.unbiased = a.spec->unbiased_scaling;
   p.scale = (float)((double)n / (double)k);  // np.float32(n / k)  (compressors.py:284)
   p.tail_shuffle = (n > 10000 && k > n / 50) ? 1 : 0;
+  p.out = out;
   p.payload = a.payload;
   p.hdr.algorithm = MC_RANDK;
   p.hdr.flags = p.unbiased ? 1u : 0u;
@@ -701,11 +1336,40 @@ int encode_randk(const EncodeArgs& a) {
   if (cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st) != cudaSuccess) return MC_ECUDA;
   if (cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st) != cudaSuccess) return MC_ECUDA;
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 256), (int64_t)sm_count() * 4));
-  note_launch(); k_sparse_prologue<<<g1, 256, 0, st>>>(p.pro, n, p.err, p.payload, p.hdr);
+  note_launch(); k_sparse_prologue<<<g1, 256, 0, st>>>(p.pro, n, p.err, p.payload, p.hdr, out);
   if (k == n) {
     note_launch(); k_bitmap_all<<<(unsigned)imax(1, imin(cdiv(nwords, 256), 1024)), 256, 0, st>>>(p);
   } else {
-    note_launch(); k_randk_walk<<<1, 32, 0, st>>>(p);
+    // the 32-bit draw stream (k + margin for rejections) in the unused candidate-list area;
+    // walk scratch after it: expectations, L_w, entering offsets, tables, control
+    const int64_t nwords = imin(n, k + k / 16 + 4096);
+    const int64_t nwin = cdiv(nwords, WP);
+    uint8_t* wsb = reinterpret_cast<uint8_t*>(p.w.list) + a16(4 * nwords);
+    double* expw = reinterpret_cast<double*>(wsb);
+    int64_t* Lw = reinterpret_cast<int64_t*>(wsb + a16(8 * nwin));
+    int64_t* tin = reinterpret_cast<int64_t*>(wsb + 2 * a16(8 * nwin));
+    WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + 3 * a16(8 * nwin));
+    uint8_t* tables = wsb + 3 * a16(8 * nwin) + 64;
+    note_launch(); k_randk_words<<<(unsigned)imax(1, imin(cdiv(nwords, 8 * 256), (int64_t)sm_count() * 4)), 256, 0, st>>>(p, p.w.list, nwords);
+    if (4 * n >= a16(4 * nwords) + 3 * a16(8 * nwin) + 64 + nwin * DW) {  // room for the parallel walk
+      static bool configured = false;
+      const int tsmem = (DW + RX) * 32 * 4;
+      if (!configured) {
+        if (cudaFuncSetAttribute(k_randk_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem) != cudaSuccess ||
+            cudaFuncSetAttribute(k_randk_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * DW) != cudaSuccess) {
+          set_error("randk walk smem configuration failed");
+          return MC_ECUDA;
+        }
+        configured = true;
+      }
+      note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
+      note_launch(); k_randk_tables<<<(unsigned)nwin, 1024, tsmem, st>>>(p, p.w.list, nwords, expw, Lw, tables);
+      note_launch(); k_randk_chain<<<1, 1024, 96 * DW, st>>>(p, Lw, tables, nwin, tin, ctl);
+      note_launch(); k_randk_emit_draws<<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);
+      note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, &ctl->fail_base);
+    } else {
+      note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, nullptr);
+    }
     if (p.tail_shuffle) {
       note_launch(); k_randk_tail_shuffle<<<1, 1, 0, st>>>(p);
     } else {
@@ -741,7 +1405,7 @@ int decode_mean_sparse(const mc_spec* s, const mc_layout& L, const uint8_t* base
   const int64_t maxcap = L.cap > 0 ? L.cap : L.n;
   dim3 g1((unsigned)imax(1, imin(cdiv(maxcap + 1, 256), (int64_t)sm_count() * 4)), (unsigned)nranks);
   note_launch(); k_sparse_starts<<<g1, 256, 0, c.stream>>>(p);
-  note_launch(); k_sparse_tiles<<<(unsigned)p.ntiles, 512, 0, c.stream>>>(p);
+  note_launch(); k_sparse_tiles<<<(unsigned)p.ntiles, 256, 0, c.stream>>>(p);
   cudaFreeAsync(scratch, c.stream);
   MC_LAUNCH_CHECK();
   return MC_OK;
