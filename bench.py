@@ -150,17 +150,21 @@ def cpu_oracle_rate(spec, gradset: str, workers: int, budget_s: float, partition
     return workers * 4.0 * D * steps / el / 1e9, el, steps
 
 
+_REF_FLAT = None  # the sample buffer, inherited by the forked workers (no pickling of data)
+
+
 def _oracle_chunk(args):
-    """Worker-process body of the reference arm: one bucket-aligned chunk."""
-    spec_doc, x, workers, seed_base = args
+    """Worker-process body of the reference arm: one bucket-aligned chunk of _REF_FLAT."""
+    spec_doc, lo, hi, workers, seed_base = args
     sys.path.insert(0, str(ROOT / "oracle"))
     import mergecomp_oracle as O
     from paper_2103_15195_b200.spec import CompressorSpec
 
     spec = CompressorSpec(**spec_doc)
+    x = _REF_FLAT[lo:hi]
     pays = [O.encode(spec, x, None, seed=O.derive_seed(seed_base, w, 0, 0))[0] for w in range(workers)]
     O.aggregate(spec, pays)
-    return len(x)
+    return hi - lo
 
 
 def run_reference(args):
@@ -176,10 +180,11 @@ def run_reference(args):
 
     from paper_2103_15195_b200 import gradsets
 
+    global _REF_FLAT
     spec = spec_for(args)
     cores = os.cpu_count() or 1
     n_workers = max(1, args.gpus)
-    flat = gradsets.synthetic_gradients(args.gradset, 0, 0)
+    flat = _REF_FLAT = gradsets.synthetic_gradients(args.gradset, 0, 0)
     D = flat.size
     B = spec.bucket_size
     budget_total = 150.0
@@ -192,7 +197,7 @@ def run_reference(args):
             jobs = []
             off = 0
             while off < sample:
-                jobs.append((spec.to_dict(), flat[off: off + chunk], n_workers, 0))
+                jobs.append((spec.to_dict(), off, min(off + chunk, sample), n_workers, 0))
                 off += chunk
             t0 = time.perf_counter()
             done = sum(pool.map(_oracle_chunk, jobs))
