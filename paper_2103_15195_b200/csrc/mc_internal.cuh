@@ -208,8 +208,10 @@ constexpr uint64_t LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_MASK = (1ull << 
 __device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
   return *reinterpret_cast<const volatile uint64_t*>(p);
 }
+// Status words are published with an atomic exchange: performed at L2, visible to every
+// polling CTA at once without a membar (which would also drain this warp's output stores).
 __device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
-  *reinterpret_cast<volatile uint64_t*>(p) = v;
+  atomicExch(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
 // Called by warp 0 of a block with its aggregate; returns the exclusive prefix in all lanes.
@@ -219,8 +221,9 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t bid,
     if (lane == 0) { st_volatile(&status[0], LB_PRE | agg); }
     return 0;
   }
+  // Flag and value travel in one 64-bit word published atomically at L2, so a reader sees
+  // either nothing or a complete entry, and no other data is published through it.
   if (lane == 0) { st_volatile(&status[bid], LB_AGG | agg); }
-  __threadfence();
   // Each step inspects a window of 32 lanes x 4 predecessors (newest first), so a block
   // that has to walk back over many aggregate-only entries (thousands of CTAs in flight)
   // pays few dependent L2 round trips.
