@@ -51,6 +51,15 @@ struct Ctx {
     }                                                                               \
   } while (0)
 
+#define MC_API_CHECK(call)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      ::mc::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return MC_ECUDA;                                                                     \
+    }                                                                                      \
+  } while (0)
+
 // --------------------------------------------------------------------------------------------
 // Philox4x64-10, counter = (block + 1, 0, 0, 0): numpy's Philox bit generator
 // (Random123 round function).  Uniform double = (w >> 11) * 2^-53.

@@ -27,6 +27,7 @@ struct SparseWS {
   uint32_t* htab;     // [2*H] hash (key, min step)
   uint32_t* bitmap;   // [ceil(n/32)]
   int64_t H;
+  int64_t bytes;  // total workspace span (single source of truth for sparse_ws_bytes)
 };
 enum { CTL_B1 = 0, CTL_KREM1, CTL_B2, CTL_KREM2, CTL_T, CTL_NEED, CTL_M, CTL_GT, CTL_COUNT, CTL_WORDS = 16 };
 
@@ -38,6 +39,7 @@ int64_t hash_size(int64_t k) {
 
 SparseWS carve(uint8_t* w, int64_t n, int64_t k) {
   SparseWS s{};
+  uint8_t* const w0 = w;
   const int64_t nblk = cdiv(n, 1024) + 1;  // finest look-back tiling in use (k_topk_final)
   s.keys = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
   s.list = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
@@ -49,6 +51,7 @@ SparseWS carve(uint8_t* w, int64_t n, int64_t k) {
   s.draws = reinterpret_cast<uint32_t*>(w); w += a16(4 * k);
   s.htab = reinterpret_cast<uint32_t*>(w); w += a16(8 * s.H);
   s.bitmap = reinterpret_cast<uint32_t*>(w); w += a16(4 * cdiv(n, 32));
+  s.bytes = (int64_t)(w - w0);
   return s;
 }
 
@@ -1218,9 +1221,7 @@ __global__ void __launch_bounds__(256) k_sparse_tiles(SD p) {
 
 int64_t sparse_ws_bytes(const mc_spec* s, int64_t n) {
   const int64_t k = s->algorithm == MC_THRESHOLD ? 1 : top_k_count(s->sparsity, n);
-  const int64_t nblk = cdiv(n, TILE) + 1;
-  return a16(4 * n) * 2 + a16(4 * (2048 + 2048 + 512)) + a16(4 * CTL_WORDS) + 16 + a16(8 * nblk) + a16(4 * k) +
-         a16(8 * hash_size(k)) + a16(4 * cdiv(n, 32)) + 64;
+  return carve(nullptr, n, k).bytes + 64;
 }
 
 static Prologue make_prologue(const EncodeArgs& a) {
@@ -1256,7 +1257,7 @@ int encode_topk(const EncodeArgs& a, float* out) {
   const int64_t ntiles = cdiv(n, CB);
   // zero histograms + ctl + ticket + status in one memset (contiguous in the carve)
   const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (ntiles + 1);
-  if (cudaMemsetAsync(p.w.hist, 0, zbytes, st) != cudaSuccess) return MC_ECUDA;
+  MC_API_CHECK(cudaMemsetAsync(p.w.hist, 0, zbytes, st));
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 1024), (int64_t)sm_count() * 8));
   note_launch(); k_topk_pass1<<<g1, 256, 0, st>>>(p);
   note_launch(); k_topk_select1<<<1, 1024, 0, st>>>(p);
@@ -1266,7 +1267,7 @@ int encode_topk(const EncodeArgs& a, float* out) {
   note_launch(); k_topk_select3<<<1, 1024, 0, st>>>(p);
   // reset ticket + status for the final look-back pass (list length <= n)
   const int64_t ftiles = cdiv(n, CB_F);
-  if (cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (ftiles + 1), st) != cudaSuccess) return MC_ECUDA;
+  MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (ftiles + 1), st));
   note_launch(); k_topk_final<<<(unsigned)imax(1, imin(ftiles, (int64_t)sm_count() * 4)), 256, 0, st>>>(p);
   MC_LAUNCH_CHECK();
   return MC_OK;
@@ -1294,7 +1295,7 @@ int encode_threshold(const EncodeArgs& a, float* out) {
   const int64_t nblk = cdiv(n, CB);
   p.ntiles = nblk;
   cudaStream_t st = a.ctx.stream;
-  if (cudaMemsetAsync(w.ticket, 0, 16 + 8 * (nblk + 1), st) != cudaSuccess) return MC_ECUDA;
+  MC_API_CHECK(cudaMemsetAsync(w.ticket, 0, 16 + 8 * (nblk + 1), st));
   const unsigned pgrid = (unsigned)imax(1, imin(nblk, (int64_t)sm_count() * 2));
   note_launch();
   if (p.pro.r) {
@@ -1332,9 +1333,9 @@ int encode_randk(const EncodeArgs& a, float* out) {
   cudaStream_t st = a.ctx.stream;
   const int64_t nwords = cdiv(n, 32);
   const int64_t nblk = cdiv(nwords, TB * 4) + 1;
-  if (cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st) != cudaSuccess) return MC_ECUDA;
-  if (cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st) != cudaSuccess) return MC_ECUDA;
-  if (cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st) != cudaSuccess) return MC_ECUDA;
+  MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st));
+  MC_API_CHECK(cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st));
+  MC_API_CHECK(cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st));
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 256), (int64_t)sm_count() * 4));
   note_launch(); k_sparse_prologue<<<g1, 256, 0, st>>>(p.pro, n, p.err, p.payload, p.hdr, out);
   if (k == n) {
