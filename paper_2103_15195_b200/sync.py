@@ -242,6 +242,75 @@ class GradSync:
         self.iteration += 1
         return host_out
 
+    # ------------------------------------------------------------ overlap with backward (WFBP)
+    def attach(self, params_backprop_order: Sequence[torch.nn.Parameter]) -> None:
+        """Bind model parameters (listed in backprop-readiness order, i.e. the profile's
+        order) to the fused buffer: every ``p.grad`` becomes a view of ``flat``, and a
+        post-accumulate-grad hook launches a group's sync on the side stream as soon as
+        its last tensor is ready — the reference simulator's FIFO channel
+        ``start_i = max(finish_{i-1}, ready_i)`` (simulator.py:114-142) on real hardware.
+        Zero gradients with ``zero_grad(set_to_none=False)`` so the views persist."""
+        params = list(params_backprop_order)
+        if [p.numel() for p in params] != self.profile.sizes():
+            raise ValueError("parameters do not match the profile sizes (backprop order)")
+        for p, g in zip(params, self.grads):
+            if p.device != self.device or p.dtype != torch.float32:
+                raise ValueError("GradSync.attach needs fp32 parameters on the sync device")
+            p.grad = g.view_as(p)
+        self._params = params
+        self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(i)) for i, p in enumerate(params)]
+        self._armed = False
+
+    def _make_hook(self, i: int):
+        def hook(_p):
+            if self._armed:
+                self._tensor_ready(i)
+        return hook
+
+    def begin_backward(self) -> None:
+        """Arm the hooks for one backward pass under the pinned partition."""
+        plan = self._plan(self.partition)
+        ranges = self.partition.group_ranges()
+        self._group_of = [g for g, (a, b) in enumerate(ranges) for _ in range(a, b)]
+        self._left = [b - a for a, b in ranges]
+        self._next_group = 0
+        self._launched = [False] * len(plan)
+        self._armed = True
+
+    def _tensor_ready(self, i: int) -> None:
+        g = self._group_of[i]
+        self._left[g] -= 1
+        # groups go out in order (one FIFO channel): launch every consecutive complete group
+        while self._next_group < len(self._left) and self._left[self._next_group] == 0:
+            self._launch_group(self._next_group)
+            self._next_group += 1
+
+    def _launch_group(self, g: int) -> None:
+        grp = self._plan(self.partition)[g]
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.device))  # the backward stream produced it
+        self.stream.wait_event(ready)
+        with torch.cuda.stream(self.stream):
+            self._sync_group(g, grp)
+        self._launched[g] = True
+
+    def finish_backward(self) -> None:
+        """Launch any group not triggered yet (e.g. tensors without gradients) and make the
+        caller's stream wait for the averaged gradients; advances the iteration."""
+        if not self._armed:
+            raise RuntimeError("finish_backward() without begin_backward()")
+        for g in range(len(self._launched)):
+            if not self._launched[g]:
+                self._launch_group(g)
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        self._armed = False
+        self.iteration += 1
+
+    def detach(self) -> None:
+        for h in getattr(self, "_hooks", []):
+            h.remove()
+        self._hooks = []
+
     def check(self) -> None:
         """Raise the reference's ValueError if any device error flag was set."""
         flags = int(self.err.item())

@@ -136,3 +136,46 @@ def test_sync_host_pipelined_equals_device_step(algo):
         for ga, gb in zip(a._plan(part), b._plan(part)):
             if ga.residual is not None:
                 assert torch.equal(ga.residual.view(torch.int64), gb.residual.view(torch.int64))
+
+
+@pytest.mark.parametrize("algo", ["efsignsgd", "dgc_lite", "qsgd"])
+def test_backward_overlap_hooks_equal_post_backward_step(algo):
+    """WFBP: groups synced from post-accumulate-grad hooks during backward produce the
+    same averaged gradients (bitwise) as one step() after backward."""
+    torchvision = pytest.importorskip("torchvision")
+    from paper_2103_15195_b200.profiles import ModelProfile, Partition
+    from paper_2103_15195_b200.spec import CompressorSpec
+    from paper_2103_15195_b200.sync import GradSync
+
+    torch.manual_seed(0)
+    torch.backends.cudnn.deterministic = True  # both backward passes must produce identical bits
+    torch.backends.cudnn.benchmark = False
+    spec = CompressorSpec(algo, sparsity=0.99)
+
+    def build():
+        torch.manual_seed(0)
+        m = torchvision.models.resnet18(weights=None).cuda()
+        params = [p for p in m.parameters() if p.requires_grad][::-1]  # backprop order
+        prof = ModelProfile.from_sizes("resnet18", [p.numel() for p in params])
+        return m, params, prof
+
+    x = torch.randn(8, 3, 64, 64, device="cuda")
+    m1, p1, prof = build()
+    m2, p2, _ = build()
+    part = Partition(prof.n_tensors, (20, 45))
+    s1 = GradSync(spec, prof, partition=part, root_seed=4)
+    s2 = GradSync(spec, prof, partition=part, root_seed=4)
+    s1.attach(p1)
+    for it in range(2):
+        m1.zero_grad(set_to_none=False)
+        s1.begin_backward()
+        m1(x).square().mean().backward()
+        s1.finish_backward()
+        m2.zero_grad(set_to_none=True)
+        m2(x).square().mean().backward()
+        s2.flat.copy_(torch.cat([p.grad.reshape(-1) for p in p2]))
+        s2.step()
+        torch.cuda.synchronize()
+        assert torch.equal(s1.flat.view(torch.int32), s2.flat.view(torch.int32)), (algo, it)
+        assert all(g1.data_ptr() == s1.flat[a:a + 1].data_ptr() for g1, a in zip([p.grad for p in p1], prof.offsets()[:-1]))
+    s1.detach()
