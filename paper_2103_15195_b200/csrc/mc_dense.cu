@@ -154,10 +154,11 @@ __device__ __forceinline__ void dec8(const DP& p, const uint8_t* pl, uint32_t e0
     if (cnt == 8) w = *reinterpret_cast<const uint64_t*>(bits + e0);
     else
       for (int q = 0; q < cnt; ++q) w |= (uint64_t)bits[e0 + q] << (8 * q);
+    const float step0 = __fdiv_rn(val[e0 / (uint32_t)p.B], 127.0f);  // s / 127 of the group's bucket
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const float s = val[SAMEB ? e0 / (uint32_t)p.B : (e0 + q) / (uint32_t)p.B];
-      d[q] = __fmul_rn((float)(int8_t)(uint8_t)(w >> (8 * q)), __fdiv_rn(s, 127.0f));  // (:513)
+      const float step = SAMEB ? step0 : __fdiv_rn(val[(e0 + q) / (uint32_t)p.B], 127.0f);
+      d[q] = __fmul_rn((float)(int8_t)(uint8_t)(w >> (8 * q)), step);  // q * (s / 127)  (:513)
     }
     return;
   }
@@ -186,6 +187,104 @@ __device__ __forceinline__ void dec8(const DP& p, const uint8_t* pl, uint32_t e0
   }
 }
 
+// acc / f32(nranks): for a power-of-two rank count the product with the exact reciprocal
+// is the same correctly rounded value as the IEEE quotient (both round the same real).
+__device__ __forceinline__ float rank_mean(float acc, float fn, float inv, bool pow2) {
+  return pow2 ? __fmul_rn(acc, inv) : __fdiv_rn(acc, fn);
+}
+
+// Sign-bit codecs (efsignsgd, onebit, signsgd/signum, 8-bit qsgd): one thread per 32-element
+// sign word, bucket_size % 32 == 0 so the word lies in one bucket; per rank one u32 of
+// signs + the bucket scale(s) (+ 32 code bytes), per element select/multiply + add.
+// qsgd's code / (L-1) comes from a 256-entry table of the exact IEEE quotients.
+template <int ALGO>
+__global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
+  __shared__ float tbl[256];
+  if (ALGO == MC_QSGD) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tbl[i] = __fdiv_rn((float)i, p.top);
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
+    const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(p.base + p.stride * threadIdx.x);
+    if (h->algorithm != p.algo || h->original_len != (uint64_t)p.n || h->n_val != p.n_val || h->n_bits != p.n_bits)
+      atomicOr(p.err, MC_ERR_HEADER);
+  }
+  const float fn = (float)p.nranks;
+  const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
+  const float inv = __fdiv_rn(1.0f, fn);
+  const uint32_t words = (uint32_t)cdiv(p.n, 32);
+  const bool vout = ((uintptr_t)p.out % 16) == 0;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    const uint32_t e0 = 32 * w;
+    const int cnt = (int)imin(32, p.n - (int64_t)e0);
+    const uint32_t b = (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) ? 0u : e0 / (uint32_t)p.B;
+    float acc[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = 0.0f;
+    // ranks in chunks of RC: all loads of a chunk are issued before any use (ILP across
+    // ranks); accumulation stays in rank order 0..n-1 (compressors.py:529-531)
+    constexpr int RC = (ALGO == MC_QSGD) ? 4 : 8;
+    for (int r0 = 0; r0 < p.nranks; r0 += RC) {
+      uint32_t sw[RC];
+      float hi[RC], lo[RC];
+      uint32_t cw[ALGO == MC_QSGD ? RC : 1][8];
+#pragma unroll
+      for (int rr = 0; rr < RC; ++rr) {
+        sw[rr] = 0;
+        hi[rr] = lo[rr] = 0.0f;
+        if (r0 + rr >= p.nranks) continue;
+        const uint8_t* pl = p.base + p.stride * (r0 + rr);
+        const float* val = reinterpret_cast<const float*>(pl + p.off_val);
+        sw[rr] = reinterpret_cast<const uint32_t*>(pl + p.off_bits)[w];
+        if (ALGO == MC_ONEBIT) { lo[rr] = val[2 * b]; hi[rr] = val[2 * b + 1]; }
+        else { hi[rr] = val[b]; }
+        if (ALGO == MC_QSGD) {
+          const uint8_t* cp = pl + p.off_codes + e0;
+          if (cnt == 32) {
+            const uint4 c0 = reinterpret_cast<const uint4*>(cp)[0], c1 = reinterpret_cast<const uint4*>(cp)[1];
+            cw[ALGO == MC_QSGD ? rr : 0][0] = c0.x; cw[ALGO == MC_QSGD ? rr : 0][1] = c0.y;
+            cw[ALGO == MC_QSGD ? rr : 0][2] = c0.z; cw[ALGO == MC_QSGD ? rr : 0][3] = c0.w;
+            cw[ALGO == MC_QSGD ? rr : 0][4] = c1.x; cw[ALGO == MC_QSGD ? rr : 0][5] = c1.y;
+            cw[ALGO == MC_QSGD ? rr : 0][6] = c1.z; cw[ALGO == MC_QSGD ? rr : 0][7] = c1.w;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              uint32_t v = 0;
+              for (int t = 0; t < 4; ++t)
+                if (4 * j + t < cnt) v |= (uint32_t)cp[4 * j + t] << (8 * t);
+              cw[ALGO == MC_QSGD ? rr : 0][j] = v;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < RC; ++rr) {
+        if (r0 + rr >= p.nranks) break;
+        if (ALGO != MC_ONEBIT) lo[rr] = __fmul_rn(-1.0f, hi[rr]);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const bool bit = (sw[rr] >> (8 * (q >> 3) + 7 - (q & 7))) & 1u;  // np.packbits order
+          float d = bit ? hi[rr] : lo[rr];
+          if (ALGO == MC_QSGD)  // (sgn * s) * (code / (L-1))
+            d = __fmul_rn(d, tbl[(cw[ALGO == MC_QSGD ? rr : 0][q >> 2] >> (8 * (q & 3))) & 0xffu]);
+          acc[q] = __fadd_rn(acc[q], d);
+        }
+      }
+    }
+    if (cnt == 32 && vout) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        reinterpret_cast<float4*>(p.out + e0)[j] =
+            make_float4(rank_mean(acc[4 * j], fn, inv, pow2), rank_mean(acc[4 * j + 1], fn, inv, pow2),
+                        rank_mean(acc[4 * j + 2], fn, inv, pow2), rank_mean(acc[4 * j + 3], fn, inv, pow2));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < cnt) p.out[e0 + q] = rank_mean(acc[q], fn, inv, pow2);
+    }
+  }
+}
+
 template <int ALGO, bool SAMEB>
 __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
   if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
@@ -194,6 +293,8 @@ __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
       atomicOr(p.err, MC_ERR_HEADER);
   }
   const float fn = (float)p.nranks;
+  const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
+  const float inv = __fdiv_rn(1.0f, fn);
   const uint32_t groups = (uint32_t)cdiv(p.n, 8);
   const bool vout = ((uintptr_t)p.out % 16) == 0;
   for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += gridDim.x * blockDim.x) {
@@ -202,6 +303,7 @@ __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
     float acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+#pragma unroll 4
     for (int r = 0; r < p.nranks; ++r) {  // rank order 0..n-1, fp32 (compressors.py:529-531)
       float d[8];
       dec8<ALGO, SAMEB>(p, p.base + p.stride * r, e0, cnt, d);
@@ -209,7 +311,7 @@ __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
       for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], d[q]);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = __fdiv_rn(acc[q], fn);
+    for (int q = 0; q < 8; ++q) acc[q] = rank_mean(acc[q], fn, inv, pow2);
     if (cnt == 8 && vout) {
       reinterpret_cast<float4*>(p.out + e0)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
       reinterpret_cast<float4*>(p.out + e0)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -280,6 +382,22 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
   const unsigned grid = (unsigned)imax(1, imin(cdiv(groups, 256), (int64_t)sm_count() * 16));
   cudaStream_t st = c.stream;
   const bool sameb = p.B % 8 == 0;
+  const int a = s->algorithm;
+  const bool sign32 = (a == MC_SIGNSGD || a == MC_SIGNUM) ||
+                      ((a == MC_EFSIGNSGD || a == MC_ONEBIT || (a == MC_QSGD && p.width == 8)) && p.B % 32 == 0);
+  if (sign32) {
+    const unsigned g32 = (unsigned)imax(1, imin(cdiv(cdiv(L.n, 32), 256), (int64_t)sm_count() * 8));
+    note_launch();
+    switch (a) {
+      case MC_SIGNSGD: k_decode_sign32<MC_SIGNSGD><<<g32, 256, 0, st>>>(p); break;
+      case MC_SIGNUM: k_decode_sign32<MC_SIGNUM><<<g32, 256, 0, st>>>(p); break;
+      case MC_EFSIGNSGD: k_decode_sign32<MC_EFSIGNSGD><<<g32, 256, 0, st>>>(p); break;
+      case MC_ONEBIT: k_decode_sign32<MC_ONEBIT><<<g32, 256, 0, st>>>(p); break;
+      default: k_decode_sign32<MC_QSGD><<<g32, 256, 0, st>>>(p); break;
+    }
+    MC_LAUNCH_CHECK();
+    return MC_OK;
+  }
 #define MC_DEC_CASE(A)                                              \
   case A:                                                           \
     note_launch();                                                  \

@@ -1205,15 +1205,18 @@ __global__ void __launch_bounds__(256) k_sparse_tiles(SD p) {
     __syncthreads();
   }
   const float fn = (float)p.nranks;
+  // power-of-two rank counts: the exact reciprocal product equals the IEEE quotient
+  const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
+  const float inv = __fdiv_rn(1.0f, fn);
+  auto mean = [&](float v) { return pow2 ? __fmul_rn(v, inv) : __fdiv_rn(v, fn); };
   const int64_t lim = imin(DT, p.n - t0);
   if (lim == DT && ((uintptr_t)(p.out + t0) % 16) == 0) {
     for (int i = threadIdx.x; i < DT / 4; i += blockDim.x) {
       const float4 v = reinterpret_cast<const float4*>(acc)[i];
-      reinterpret_cast<float4*>(p.out + t0)[i] =
-          make_float4(__fdiv_rn(v.x, fn), __fdiv_rn(v.y, fn), __fdiv_rn(v.z, fn), __fdiv_rn(v.w, fn));
+      reinterpret_cast<float4*>(p.out + t0)[i] = make_float4(mean(v.x), mean(v.y), mean(v.z), mean(v.w));
     }
   } else {
-    for (int i = threadIdx.x; i < lim; i += blockDim.x) p.out[t0 + i] = __fdiv_rn(acc[i], fn);
+    for (int i = threadIdx.x; i < lim; i += blockDim.x) p.out[t0 + i] = mean(acc[i]);
   }
 }
 

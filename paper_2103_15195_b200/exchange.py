@@ -32,27 +32,33 @@ def world(group=None) -> tuple[int, int]:
     return 0, 1
 
 
-def _gather_into(out: torch.Tensor, inp: torch.Tensor, group=None) -> None:
+def _gather_into(out: torch.Tensor, inp: torch.Tensor, group=None, async_op: bool = False):
     """all_gather_into_tensor; CUDA tensors on a gloo group are staged through host
-    memory (lets several ranks share one GPU in tests — NCCL is the production path)."""
+    memory (lets several ranks share one GPU in tests — NCCL is the production path).
+    With ``async_op`` (NCCL) returns the work handle; the caller's stream must ``wait()``
+    on it before reading ``out``."""
     if inp.is_cuda and dist.get_backend(group) == "gloo":
         host = torch.empty(out.numel(), dtype=out.dtype)
         dist.all_gather_into_tensor(host, inp.cpu(), group=group)
         out.copy_(host)
-    else:
-        dist.all_gather_into_tensor(out, inp, group=group)
+        return None
+    return dist.all_gather_into_tensor(out, inp, group=group, async_op=async_op)
 
 
-def allgather_fixed(payload: torch.Tensor, out: Optional[torch.Tensor] = None, group=None) -> tuple[torch.Tensor, int]:
-    """Gather equal-size uint8 payload buffers; returns (gathered, stride)."""
+def allgather_fixed(payload: torch.Tensor, out: Optional[torch.Tensor] = None, group=None,
+                    async_op: bool = False):
+    """Gather equal-size uint8 payload buffers; returns (gathered, stride) — or
+    (gathered, stride, work) with ``async_op`` (work is None when already complete)."""
     _, n = world(group)
     stride = payload.numel()
+    work = None
     if n == 1:
-        return payload, stride
-    if out is None:
-        out = torch.empty(n * stride, dtype=torch.uint8, device=payload.device)
-    _gather_into(out, payload, group)
-    return out, stride
+        out = payload
+    else:
+        if out is None:
+            out = torch.empty(n * stride, dtype=torch.uint8, device=payload.device)
+        work = _gather_into(out, payload, group, async_op=async_op)
+    return (out, stride, work) if async_op else (out, stride)
 
 
 def read_count(payload: torch.Tensor) -> torch.Tensor:

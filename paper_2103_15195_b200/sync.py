@@ -166,15 +166,47 @@ class GradSync:
 
     def step(self, partition: Optional[Partition] = None) -> None:
         """One synchronisation of every group of ``partition`` (default: the pinned one),
-        enqueued on the side stream after the gradients' producer stream."""
+        enqueued on the side stream after the gradients' producer stream.
+
+        With several ranks and fixed-size payloads the groups are pipelined: every
+        group's encode is followed by an asynchronous allgather, and the decodes wait on
+        their own gather only — encode(g+1) runs while allgather(g) is on NVLink (the
+        compute and communication channels of MergeComp, simulator.py:114-142)."""
         part = self.partition if partition is None else self._resolve(partition)
         plan = self._plan(part)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
-            for g, grp in enumerate(plan):
-                self._sync_group(g, grp)
+            if self.world > 1 and self.spec.algorithm != "threshold" and len(plan) > 1:
+                pending = []
+                for g, grp in enumerate(plan):
+                    x = self._encode_group(g, grp)
+                    gathered, stride, work = exchange.allgather_fixed(grp.payload, grp.gather, group=self.pg,
+                                                                      async_op=True)
+                    pending.append((grp, x, gathered, stride, work))
+                for grp, x, gathered, stride, work in pending:
+                    if work is not None:
+                        work.wait()  # side stream waits for this group's gather only
+                    device_decode_mean(self.spec, gathered, stride, self.world, grp.n, x, self.err,
+                                       stream=self.stream, cspec=self.cspec)
+            else:
+                for g, grp in enumerate(plan):
+                    self._sync_group(g, grp)
         torch.cuda.current_stream(self.device).wait_stream(self.stream)
         self.iteration += 1
+
+    def _encode_group(self, g: int, grp: _Group) -> torch.Tensor:
+        lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
+        x = self.flat[grp.start:grp.end]
+        probe = self.probe is not None and self.probe[0] == g
+        if probe:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(self.stream)
+        device_encode(self.spec, x, grp.residual, grp.momentum, lo | (hi << 64), out=grp.payload,
+                      err=self.err, stream=self.stream, cspec=self.cspec)
+        if probe:
+            ev[1].record(self.stream)
+            self.probe[1].append(ev)
+        return x
 
     CHUNKABLE = frozenset({"identity", "fp16", "efsignsgd", "onebit", "int8"})
 

@@ -1,0 +1,59 @@
+"""Per-GPU sync-step time at N ranks, measured on ONE B200 for the parts this repo
+owns: encode (unfused, payload only) + decode_mean over N gathered payloads (the N
+payloads of N different gradient sets stacked exactly like the NCCL allgather
+output).  The allgather itself is estimated from the payload size and the measured
+peer bandwidth (770 GB/s per direction, B200_PROFILING.md); (N-1) * P bytes arrive
+per rank.  Prints one JSON line per (codec, N)."""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2103_15195_b200 import compressors as C, gradsets  # noqa: E402
+from paper_2103_15195_b200.spec import CompressorSpec  # noqa: E402
+
+
+def timed(fn, reps=20):
+    for _ in range(3):
+        fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gradset", default="resnet50_161")
+    ap.add_argument("--codecs", default="efsignsgd,onebit,dgc_lite,qsgd,terngrad,int8,fp16")
+    a = ap.parse_args()
+    D = sum(gradsets.sizes(a.gradset))
+    grads = [torch.from_numpy(gradsets.synthetic_gradients(a.gradset, 0, r)).cuda() for r in range(8)]
+    for name in a.codecs.split(","):
+        spec = CompressorSpec(name, sparsity=0.999 if name in ("topk", "dgc_lite") else 0.99)
+        res = torch.zeros(D, dtype=torch.float64, device="cuda") if spec.uses_error_feedback else None
+        pays = [C.device_encode(spec, g, None if res is None else res.clone(), None, 1) for g in grads]
+        stride = pays[0].buf.numel()
+        gathered = torch.cat([p.buf for p in pays])
+        out = torch.empty(D, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        x = grads[0].clone()
+        t_enc = timed(lambda: C.device_encode(spec, x, res, None, 1, out=pays[0].buf))
+        P = C.payload_bytes(spec, D)
+        for N in (1, 2, 4, 8):
+            t_dec = timed(lambda: C.device_decode_mean(spec, gathered, stride, N, D, out, err))
+            t_ag = (N - 1) * P / 770e9 * 1e3
+            step = t_enc + t_ag + t_dec
+            print(json.dumps({"codec": name, "N": N, "encode_ms": round(t_enc, 4), "decode_mean_ms": round(t_dec, 4),
+                              "allgather_est_ms": round(t_ag, 4), "step_ms": round(step, 4),
+                              "per_gpu_GBps": round(4 * D / step / 1e6, 1)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
