@@ -4,6 +4,8 @@
 // decode_mean: one thread owns 8 consecutive elements (one sign byte per rank); for
 // r = 0..nranks-1 it decodes payload r and accumulates acc = fl32(acc + d_r) starting
 // from +0.0f, then writes acc / f32(nranks) — the reference's float32 order exactly.
+#include <cstdlib>
+
 #include "mc_internal.cuh"
 
 namespace mc {
@@ -200,6 +202,7 @@ __device__ __forceinline__ float rank_mean(float acc, float fn, float inv, bool 
 template <int ALGO>
 __global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
   __shared__ float tbl[256];
+  __shared__ __align__(16) float s_out[8][32 * 36];
   if (ALGO == MC_QSGD) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) tbl[i] = __fdiv_rn((float)i, p.top);
     __syncthreads();
@@ -214,9 +217,14 @@ __global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
   const float inv = __fdiv_rn(1.0f, fn);
   const uint32_t words = (uint32_t)cdiv(p.n, 32);
   const bool vout = ((uintptr_t)p.out % 16) == 0;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  float* so = s_out[threadIdx.x >> 5];
+  // warp-uniform loop: lane l owns word wb + l (32 consecutive words = 1024 elements)
+  for (uint32_t wb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wb < words; wb += gridDim.x * blockDim.x) {
+    const uint32_t w = wb + lane;
+    const bool live = w < words;
     const uint32_t e0 = 32 * w;
-    const int cnt = (int)imin(32, p.n - (int64_t)e0);
+    const int cnt = live ? (int)imin(32, p.n - (int64_t)e0) : 0;
     const uint32_t b = (ALGO == MC_SIGNSGD || ALGO == MC_SIGNUM) ? 0u : e0 / (uint32_t)p.B;
     float acc[32];
 #pragma unroll
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
       for (int rr = 0; rr < RC; ++rr) {
         sw[rr] = 0;
         hi[rr] = lo[rr] = 0.0f;
-        if (r0 + rr >= p.nranks) continue;
+        if (r0 + rr >= p.nranks || !live) continue;
         const uint8_t* pl = p.base + p.stride * (r0 + rr);
         const float* val = reinterpret_cast<const float*>(pl + p.off_val);
         sw[rr] = reinterpret_cast<const uint32_t*>(pl + p.off_bits)[w];
@@ -271,12 +279,22 @@ __global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
         }
       }
     }
-    if (cnt == 32 && vout) {
+    if (__all_sync(FULL, cnt == 32) && vout) {
+      // transpose through shared memory (rows of 36 floats: conflict-free float4 in and
+      // out) so each warp-wide store is one contiguous 512-byte row of the output
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        reinterpret_cast<float4*>(p.out + e0)[j] =
+        *reinterpret_cast<float4*>(so + 36 * lane + 4 * j) =
             make_float4(rank_mean(acc[4 * j], fn, inv, pow2), rank_mean(acc[4 * j + 1], fn, inv, pow2),
                         rank_mean(acc[4 * j + 2], fn, inv, pow2), rank_mean(acc[4 * j + 3], fn, inv, pow2));
+      __syncwarp();
+      float* ob = p.out + (int64_t)32 * wb;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int idx = 128 * j + 4 * lane;
+        reinterpret_cast<float4*>(ob)[32 * j + lane] = *reinterpret_cast<const float4*>(so + 36 * (idx >> 5) + (idx & 31));
+      }
+      __syncwarp();
     } else {
 #pragma unroll
       for (int q = 0; q < 32; ++q)

@@ -3,7 +3,8 @@
 // The single scaler is np.abs(x).mean() over the WHOLE group: numpy's float32 pairwise
 // tree over n elements.  Every node at depth < D of that tree is internal (longer than
 // 128) when P >> (D-1) >= 17 with P = n/8, and node offsets are multiples of 8, so:
-//   pass 1  one warp per depth-D node (<= ~800 elements): the node's [offset, length) is
+//   pass 1  one warp per depth-D node (<= 512, or 1024 for groups > 117M elements): the
+//           node's [offset, length) is
 //           found by descending the numpy split rule from the root; the warp streams the
 //           node once (momentum update, EF correction, sign bytes), stages |c32| in smem
 //           and evaluates the node's bounded pairwise tree; the 8 warps of a CTA then
@@ -17,7 +18,7 @@ namespace mc {
 namespace {
 
 constexpr int SW = 8;  // warps (nodes) per CTA in pass 1
-constexpr int NODE_MAX = 1024;
+constexpr int NODE_MAX = 1024;  // longest node the pass-1 kernels stage (8 chunks of 128)
 
 struct SP {
   Prologue pro;
@@ -31,39 +32,113 @@ struct SP {
   mc_payload_header hdr;
 };
 
+// smem position of node element q: 8 pad floats per 32 so the (typically 4) leaves that the
+// pairwise pass reads at once, ~n/4 apart, fall into disjoint bank octets; float4 aligned
+__device__ __forceinline__ int spos(int q) { return q + 8 * (q >> 5); }
+
 // Streams node `node` (depth D) once; returns the node's pairwise sum (all lanes).
-__device__ __forceinline__ float sign_node(const SP& p, int64_t node, float* a) {
+// Nodes start at multiples of 8 elements (so at sign-byte boundaries and 32-byte
+// aligned) and hold <= 128*NCH elements: every lane issues all of its float4 loads of a
+// group of 4 chunks before it touches any of them (one HBM round trip per group, not one
+// per 32 elements), then writes sign bytes, the signum momentum, and |c32| to smem.
+// MOM / EF are compile-time so the common signsgd node is a lean load/compare/store loop.
+template <int NCH, bool MOM, bool EF, bool VEC>
+__device__ __forceinline__ float sign_node(const SP& p, int node, float* a) {
   const int lane = threadIdx.x & 31;
-  int64_t off = 0, len = p.n;
+  int off = 0, len = (int)p.n;  // groups are < 2^31 elements (NODE_MAX check at launch)
   for (int d = p.D - 1; d >= 0; --d) {  // bit d of the node index = right child at that level
-    int64_t m = len / 2;
-    m -= m % 8;
+    const int m = (len >> 1) & ~7;      // n2 = n/2 - (n/2) % 8
     if ((node >> d) & 1) { off += m; len -= m; }
     else len = m;
   }
-  bool bad = false;
-  for (int64_t q0 = 0; q0 < len; q0 += 32) {
-    const int64_t q = q0 + lane;
-    float c32 = 0.0f;
-    if (q < len) {
-      p.pro.load(off + q, c32, bad, true);
-      a[q] = fabsf(c32);
+  const int L = len;
+  const float* g = p.pro.g + off;
+  float* mo = MOM ? p.pro.m + off : nullptr;
+  const double* r = EF ? p.pro.r + off : nullptr;
+  float nanacc = 0.0f;  // x * 0 + acc stays 0 unless some x is inf / nan
+#pragma unroll
+  for (int c0 = 0; c0 < NCH; c0 += 4) {
+    float xv[4][4], mv[4][4];
+    double rv[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q0 = 128 * (c0 + i) + 4 * lane;
+      if (VEC && q0 + 3 < L) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(g + q0));
+        xv[i][0] = v.x; xv[i][1] = v.y; xv[i][2] = v.z; xv[i][3] = v.w;
+        if (MOM) {
+          const float4 u = *reinterpret_cast<const float4*>(mo + q0);
+          mv[i][0] = u.x; mv[i][1] = u.y; mv[i][2] = u.z; mv[i][3] = u.w;
+        }
+        if (EF) {
+          const double2 r0 = *reinterpret_cast<const double2*>(r + q0);
+          const double2 r1 = *reinterpret_cast<const double2*>(r + q0 + 2);
+          rv[i][0] = r0.x; rv[i][1] = r0.y; rv[i][2] = r1.x; rv[i][3] = r1.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = q0 + k < L;
+          xv[i][k] = in ? g[q0 + k] : 0.0f;
+          if (MOM) mv[i][k] = in ? mo[q0 + k] : 0.0f;
+          if (EF) rv[i][k] = in ? r[q0 + k] : 0.0;
+        }
+      }
     }
-    const unsigned m = __ballot_sync(FULL, q < len && c32 >= 0.0f);  // bit = x >= 0
-    if (lane < 4 && q0 + 8 * lane < len)  // elements 8*lane .. +7 of this chunk, MSB first
-      p.signs[(off + q0) / 8 + lane] = (uint8_t)((__brev(m) >> (24 - 8 * lane)) & 0xffu);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q0 = 128 * (c0 + i) + 4 * lane;
+      if (c0 + i > 0 && 128 * (c0 + i) >= L) break;  // warp-uniform: node ends before this chunk
+      float c32[4];
+      uint32_t nib = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = xv[i][k];
+        nanacc = __fmaf_rn(x, 0.0f, nanacc);
+        float w = x;
+        if (MOM) {  // signum / momentum (compressors.py:402-405)
+          w = p.pro.signum ? __fadd_rn(__fmul_rn(p.pro.beta, mv[i][k]), __fmul_rn(p.pro.omb, x))
+                           : __fadd_rn(__fmul_rn(p.pro.beta, mv[i][k]), x);
+          mv[i][k] = w;
+        }
+        c32[k] = EF ? __double2float_rn(__dadd_rn((double)w, rv[i][k])) : w;
+        nib |= (uint32_t)(c32[k] >= 0.0f) << (3 - k);  // bit = x >= 0, MSB first
+      }
+      const bool full = q0 + 3 < L;
+      if (!full) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (q0 + k >= L) nib &= ~(1u << (3 - k));  // np.packbits pads with zero bits
+      }
+      if (MOM) {
+        if (VEC && full) {
+          *reinterpret_cast<float4*>(mo + q0) = make_float4(mv[i][0], mv[i][1], mv[i][2], mv[i][3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (q0 + k < L) mo[q0 + k] = mv[i][k];
+        }
+      }
+      // |c32| for the pairwise tree; lanes past the node end store zeros nobody reads
+      *reinterpret_cast<float4*>(a + spos(q0)) = make_float4(fabsf(c32[0]), fabsf(c32[1]), fabsf(c32[2]), fabsf(c32[3]));
+      // lanes 2j, 2j+1 hold the high / low nibble of sign byte j of this chunk
+      uint32_t byte = nib << ((lane & 1) ? 0 : 4);
+      byte |= __shfl_xor_sync(FULL, byte, 1);
+      if (!(lane & 1) && q0 < L) p.signs[(off + q0) >> 3] = (uint8_t)byte;
+    }
   }
-  flag(p.err, bad, MC_ERR_NONFINITE);
+  flag(p.err, nanacc != 0.0f, MC_ERR_NONFINITE);
   __syncwarp();
-  return warp_pairwise_small<4>([&](int q) { return a[q]; }, (int)len);
+  return warp_pairwise_small<3>([&](int q) { return a[spos(q)]; }, L);
 }
 
+template <int NCH, bool MOM, bool EF, bool VEC>
 __global__ void __launch_bounds__(SW * 32) k_sign_nodes(SP p) {
-  __shared__ __align__(16) float sm[SW][NODE_MAX];
+  __shared__ __align__(16) float sm[SW][160 * NCH];
   __shared__ float s_node[SW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
-  const float s = sign_node(p, (int64_t)blockIdx.x * SW + warp, sm[warp]);
+  const float s = sign_node<NCH, MOM, EF, VEC>(p, (int)blockIdx.x * SW + warp, sm[warp]);
   if (lane == 0) s_node[warp] = s;
   __syncthreads();
   if (threadIdx.x == 0) {  // nodes 8b .. 8b+7 form a perfect subtree (3 levels)
@@ -74,11 +149,32 @@ __global__ void __launch_bounds__(SW * 32) k_sign_nodes(SP p) {
 }
 
 // small trees (D < 3): one warp per node
+template <bool MOM, bool EF>
 __global__ void k_sign_nodes_small(SP p) {
-  __shared__ __align__(16) float sm[NODE_MAX];
+  __shared__ __align__(16) float sm[160 * 8];
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
-  const float s = sign_node(p, blockIdx.x, sm);
+  const float s = sign_node<8, MOM, EF, false>(p, blockIdx.x, sm);
   if (threadIdx.x == 0) p.partial[blockIdx.x] = s;
+}
+
+template <bool MOM, bool EF>
+void launch_nodes(const SP& p, int64_t n, int64_t nodes, cudaStream_t st) {
+  // node offsets are multiples of 8 elements: 16-byte aligned bases keep every node aligned
+  const bool vec = (uintptr_t)p.pro.g % 16 == 0 && (!MOM || (uintptr_t)p.pro.m % 16 == 0) &&
+                   (!EF || (uintptr_t)p.pro.r % 16 == 0);
+  if (p.D >= 3) {
+    // longest node at depth D is < (n >> D) + 8 (each split leaves the right child <= len/2 + 8)
+    const dim3 grid((unsigned)(nodes / SW));
+    if ((n >> p.D) + 16 <= 512) {
+      if (vec) k_sign_nodes<4, MOM, EF, true><<<grid, SW * 32, 0, st>>>(p);
+      else k_sign_nodes<4, MOM, EF, false><<<grid, SW * 32, 0, st>>>(p);
+    } else {
+      if (vec) k_sign_nodes<8, MOM, EF, true><<<grid, SW * 32, 0, st>>>(p);
+      else k_sign_nodes<8, MOM, EF, false><<<grid, SW * 32, 0, st>>>(p);
+    }
+  } else {
+    k_sign_nodes_small<MOM, EF><<<(unsigned)nodes, 32, 0, st>>>(p);
+  }
 }
 
 // perfect binary tree over m = 2^k values, in place with doubling strides:
@@ -109,7 +205,7 @@ int depth_for(int64_t n) {
   const int64_t P = n / 8;
   int D = 0;
   // every node at depth < D is split (length > 128); stop once nodes are <= ~800 elements
-  while (D < 18 && (P >> D) >= 17 && (n >> D) > 768) ++D;
+  while (D < 18 && (P >> D) >= 17 && (n >> D) > 448) ++D;
   return D;
 }
 
@@ -145,13 +241,11 @@ int encode_sign_global(const EncodeArgs& a) {
   const int64_t nodes = 1ll << p.D;
   int m;
   note_launch();
-  if (p.D >= 3) {
-    k_sign_nodes<<<(unsigned)(nodes / SW), SW * 32, 0, st>>>(p);
-    m = (int)(nodes / SW);
-  } else {
-    k_sign_nodes_small<<<(unsigned)nodes, 32, 0, st>>>(p);
-    m = (int)nodes;
-  }
+  if (p.pro.m && p.pro.r) launch_nodes<true, true>(p, a.n, nodes, st);
+  else if (p.pro.m) launch_nodes<true, false>(p, a.n, nodes, st);
+  else if (p.pro.r) launch_nodes<false, true>(p, a.n, nodes, st);
+  else launch_nodes<false, false>(p, a.n, nodes, st);
+  m = (int)(p.D >= 3 ? nodes / SW : nodes);
   const int smem = 4 * m;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(k_sign_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
