@@ -17,7 +17,10 @@ constexpr int TILE = TB * ITEMS;
 // ------------------------------------------------------------------ workspace layout
 struct SparseWS {
   uint32_t* keys;     // [n]  float bits of the corrected c32
-  uint32_t* list;     // [n]  ordered candidate indices
+  uint32_t* list;     // [n]  top-k: per-tile candidate segments (tile t's at its first element); randk scratch
+  uint32_t* list2;    // [n]  top-k: the segments concatenated in order (the candidate list)
+  uint32_t* segcnt;   // [ntiles + 1] top-k: candidates per pass-2 tile, then their exclusive prefix
+  uint32_t* cmax;     // [ceil(n/128)] top-k: max |c32| key per 128-element chunk
   uint32_t* hist;     // [2048 + 2048 + 512]
   uint32_t* ctl;      // control words (see CTL_*)
   uint32_t* ticket;   // look-back ticket(s)
@@ -29,7 +32,8 @@ struct SparseWS {
   int64_t H;
   int64_t bytes;  // total workspace span (single source of truth for sparse_ws_bytes)
 };
-enum { CTL_B1 = 0, CTL_KREM1, CTL_B2, CTL_KREM2, CTL_T, CTL_NEED, CTL_M, CTL_GT, CTL_COUNT, CTL_WORDS = 16 };
+enum { CTL_B1 = 0, CTL_KREM1, CTL_B2, CTL_KREM2, CTL_T, CTL_NEED, CTL_M, CTL_GT, CTL_COUNT,
+       CTL_DONE1, CTL_DONE2, CTL_DONE3, CTL_WORDS = 16 };
 
 int64_t hash_size(int64_t k) {
   int64_t h = 1024;
@@ -43,6 +47,9 @@ SparseWS carve(uint8_t* w, int64_t n, int64_t k) {
   const int64_t nblk = cdiv(n, 1024) + 1;  // finest look-back tiling in use (k_topk_final)
   s.keys = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
   s.list = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
+  s.list2 = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
+  s.segcnt = reinterpret_cast<uint32_t*>(w); w += a16(4 * (cdiv(n, 8192) + 1));
+  s.cmax = reinterpret_cast<uint32_t*>(w); w += a16(4 * cdiv(n, 128));
   s.hist = reinterpret_cast<uint32_t*>(w); w += a16(4 * (2048 + 2048 + 512));
   s.ctl = reinterpret_cast<uint32_t*>(w); w += a16(4 * CTL_WORDS);
   s.ticket = reinterpret_cast<uint32_t*>(w); w += 16;
@@ -85,6 +92,18 @@ __device__ __forceinline__ uint64_t block_exscan(uint64_t v, uint64_t* total) {
   return r;
 }
 
+// true in every thread of the last CTA of the grid to get here; the fences make all
+// CTAs' earlier global writes (histogram atomics, counts) visible to it
+__device__ __forceinline__ bool last_cta(uint32_t* counter) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
 __device__ __forceinline__ int64_t take_ticket(uint32_t* ticket) {
   __shared__ int64_t s_bid;
   if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
@@ -125,9 +144,23 @@ struct TP {
   float* val_out;
   float* out;  // fused single-rank decode target (may alias g) or null
   int vec;
+  int ksrc;  // where c32 lives after pass 1: KS_R (fp64 residual), KS_F (momentum or gradient), KS_KEYS
+  const float* kf;
   uint8_t* payload;
   mc_payload_header hdr;
 };
+enum { KS_KEYS = 0, KS_R = 1, KS_F = 2 };
+
+// float bits of element e's corrected c32 (pass 1 leaves it recoverable: the EF residual
+// holds c, the momentum buffer / gradient holds w); keys are only materialised when the
+// fused output would overwrite the gradient they come from
+__device__ __forceinline__ uint32_t key_at(const TP& p, int64_t e) {
+  if (p.ksrc == KS_R) return __float_as_uint(__double2float_rn(p.pro.r[e]));
+  if (p.ksrc == KS_F) return __float_as_uint(p.kf[e]);
+  return p.w.keys[e];
+}
+
+__device__ void select_bin(const uint32_t* hist, int nb, uint32_t k, uint32_t* out_bin, uint32_t* out_krem);
 
 __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
   __shared__ uint32_t h[2048];
@@ -178,8 +211,15 @@ __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
       key[q] = __float_as_uint(c32);
       if (in) atomicAdd(&h[(key[q] & 0x7fffffffu) >> 20], 1u);
     }
+    {  // the warp's 128 consecutive elements form one chunk: record their max magnitude key
+      uint32_t km = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) km = max(km, (e0 + q < p.n) ? (key[q] & 0x7fffffffu) : 0u);
+      km = __reduce_max_sync(__activemask(), km);
+      if ((threadIdx.x & 31) == 0) p.w.cmax[e0 >> 7] = km;
+    }
     if (full) {
-      *reinterpret_cast<uint4*>(p.w.keys + e0) = make_uint4(key[0], key[1], key[2], key[3]);
+      if (p.ksrc == KS_KEYS) *reinterpret_cast<uint4*>(p.w.keys + e0) = make_uint4(key[0], key[1], key[2], key[3]);
       if (p.pro.m) *reinterpret_cast<float4*>(p.pro.m + e0) = make_float4(mo[0], mo[1], mo[2], mo[3]);
       if (p.pro.r) {  // residual of unselected elements = c  (compressors.py:412)
         *reinterpret_cast<double2*>(p.pro.r + e0) = make_double2(c[0], c[1]);
@@ -190,7 +230,7 @@ __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (e0 + q < p.n) {
-          p.w.keys[e0 + q] = key[q];
+          if (p.ksrc == KS_KEYS) p.w.keys[e0 + q] = key[q];
           if (p.pro.m) p.pro.m[e0 + q] = mo[q];
           if (p.pro.r) p.pro.r[e0 + q] = c[q];
           if (p.out) p.out[e0 + q] = 0.0f;
@@ -201,6 +241,12 @@ __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
   __syncthreads();
   for (int i = threadIdx.x; i < 2048; i += blockDim.x)
     if (h[i]) atomicAdd(&p.w.hist[i], h[i]);
+  if (last_cta(&p.w.ctl[CTL_DONE1])) {  // select1: the bin holding the k-th largest
+    __shared__ uint32_t s_b, s_r;
+    select_bin(p.w.hist, 2048, (uint32_t)p.k, &s_b, &s_r);
+    __syncthreads();
+    if (threadIdx.x == 0) { p.w.ctl[CTL_B1] = s_b; p.w.ctl[CTL_KREM1] = s_r; }
+  }
 }
 
 // find the bin holding the k-th largest: scans nb bins from the top (one CTA of 1024)
@@ -240,9 +286,6 @@ __device__ void select_bin(const uint32_t* hist, int nb, uint32_t k, uint32_t* o
   }
 }
 
-__global__ void k_topk_select1(TP p) {
-  select_bin(p.w.hist, 2048, (uint32_t)p.k, &p.w.ctl[CTL_B1], &p.w.ctl[CTL_KREM1]);
-}
 
 // Warp-chunk ordered compaction helper: given this lane's keep bits (bit 4 i + q for
 // element 128 i + 4 lane + q of the warp chunk), returns this lane's base position for
@@ -290,84 +333,139 @@ __device__ __forceinline__ uint64_t cta_chunk_prefix(uint64_t warp_total, uint64
   return r;
 }
 
-// Persistent: each CTA claims tiles in ticket order until none remain, so the look-back
-// frontier stays close behind (a one-shot grid makes a whole wave walk back at once).
-__global__ void __launch_bounds__(256) k_topk_pass2(TP p, int64_t ntiles) {
+// pass 2: one CTA per 8192-element tile compacts the tile's candidates (bin >= B1), in
+// element order, into the tile's own segment of `list` (starting at the tile's first
+// element, so it always fits) and records the count — no ordering between tiles (a
+// look-back chain over 12K tiles costs more than the whole read).  Only 128-element chunks
+// whose pass-1 maximum reaches bin B1 are read at all.
+__global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
   __shared__ uint32_t h2[2048];
+  __shared__ uint32_t s_wt[8];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) h2[i] = 0;
-  const uint32_t B1 = p.w.ctl[CTL_B1];
+  const uint32_t B1 = p.w.ctl[CTL_B1], thr = B1 << 20;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  while (true) {
-    const int64_t bid = take_ticket(p.w.ticket);
-    if (bid >= ntiles) break;
-    const int64_t c0 = bid * CB + (int64_t)warp * CW;
-    uint32_t keep = 0;
-    uint32_t kk[8][4];
+  const int64_t bid = blockIdx.x;
+  const int64_t nchunks = cdiv(p.n, 128);
+  const int64_t c0 = bid * CB + (int64_t)warp * CW;
+  const int64_t ch0 = c0 >> 7;  // this warp's 8 chunks
+  const uint32_t cm = (lane < 8 && ch0 + lane < nchunks) ? p.w.cmax[ch0 + lane] : 0u;
+  const uint32_t live = __ballot_sync(FULL, lane < 8 && ch0 + lane < nchunks && cm >= thr) & 0xffu;
+  uint32_t kk[8][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t e0 = c0 + 128 * i + 4 * lane;
-      if (e0 + 3 < p.n) {
-        const uint4 v = *reinterpret_cast<const uint4*>(p.w.keys + e0);
-        kk[i][0] = v.x; kk[i][1] = v.y; kk[i][2] = v.z; kk[i][3] = v.w;
+  for (int i = 0; i < 8; ++i) {
+    const int64_t e0 = c0 + 128 * i + 4 * lane;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) kk[i][q] = 0u;
+    if (!((live >> i) & 1u)) continue;
+    if (p.vec && e0 + 3 < p.n && p.ksrc != KS_KEYS) {
+      if (p.ksrc == KS_R) {
+        const double2 a = *reinterpret_cast<const double2*>(p.pro.r + e0), b = *reinterpret_cast<const double2*>(p.pro.r + e0 + 2);
+        kk[i][0] = __float_as_uint(__double2float_rn(a.x)); kk[i][1] = __float_as_uint(__double2float_rn(a.y));
+        kk[i][2] = __float_as_uint(__double2float_rn(b.x)); kk[i][3] = __float_as_uint(__double2float_rn(b.y));
       } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) kk[i][q] = (e0 + q < p.n) ? p.w.keys[e0 + q] : 0u;
+        const float4 v = *reinterpret_cast<const float4*>(p.kf + e0);
+        kk[i][0] = __float_as_uint(v.x); kk[i][1] = __float_as_uint(v.y);
+        kk[i][2] = __float_as_uint(v.z); kk[i][3] = __float_as_uint(v.w);
       }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (c0 + 128 * i + 4 * lane + q >= p.n) continue;
-        const uint32_t key = kk[i][q] & 0x7fffffffu, b1 = key >> 20;
-        if (b1 >= B1) keep |= 1u << (4 * i + q);
-        if (b1 == B1) atomicAdd(&h2[(key >> 9) & 0x7ffu], 1u);
-      }
-    uint32_t base[8];
-    const uint32_t wtot = warp_chunk_offsets(keep, base);
-    uint64_t tile_total;
-    const uint64_t pos0 = cta_chunk_prefix(wtot, p.w.status, bid, tile_total);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      uint32_t pos = (uint32_t)(pos0 + base[i]);
+    } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (keep & (1u << (4 * i + q))) p.w.list[pos++] = (uint32_t)(c0 + 128 * i + 4 * lane + q);
+        if (e0 + q < p.n) kk[i][q] = key_at(p, e0 + q);
     }
-    if (bid == ntiles - 1 && threadIdx.x == 0) p.w.ctl[CTL_M] = (uint32_t)(pos0 + tile_total);  // list length
   }
+  __syncthreads();  // h2 zeroed
+  uint32_t keep = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (!((live >> i) & 1u)) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t key = kk[i][q] & 0x7fffffffu;
+      const bool in = c0 + 128 * i + 4 * lane + q < p.n;
+      keep |= (uint32_t)(in && key >= thr) << (4 * i + q);
+      if (in && (key >> 20) == B1) atomicAdd(&h2[(key >> 9) & 0x7ffu], 1u);
+    }
+  }
+  const uint32_t wtot = __reduce_add_sync(FULL, __popc(keep));
+  if (lane == 0) s_wt[warp] = wtot;
   __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    before += (w < warp) ? s_wt[w] : 0;
+    tot += s_wt[w];
+  }
+  if (wtot) {
+    uint32_t base[8];
+    warp_chunk_offsets(keep, base);
+    uint32_t* seg = p.w.list + bid * CB;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t pos = before + base[i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (keep & (1u << (4 * i + q))) seg[pos++] = (uint32_t)(c0 + 128 * i + 4 * lane + q);
+    }
+  }
+  if (threadIdx.x == 0) p.w.segcnt[bid] = tot;
   for (int i = threadIdx.x; i < 2048; i += blockDim.x)
     if (h2[i]) atomicAdd(&p.w.hist[2048 + i], h2[i]);
 }
 
-__global__ void k_topk_select2(TP p) {
-  select_bin(p.w.hist + 2048, 2048, p.w.ctl[CTL_KREM1], &p.w.ctl[CTL_B2], &p.w.ctl[CTL_KREM2]);
-}
-
-// histogram of the low 9 key bits over list entries in (B1, B2)
-__global__ void k_topk_hist3(TP p) {
+// hist3: every CTA turns the pass-2 tile counts into their exclusive prefix in shared
+// memory (one coalesced L2 read of ntiles words) and resolves select2 itself; then, grid-
+// stride over list positions (a position's tile by binary search in smem, so one crowded
+// tile does not serialise on one CTA), it concatenates the tile segments into list2 (the
+// ordered candidate list) and histograms the low 9 key bits of the entries inside
+// (B1, B2).  The last CTA resolves select3 (the exact threshold key T and the tie quota).
+constexpr int64_t H3_MAX_TILES = 48 * 1024;  // 192 KB of prefix in smem: groups <= 402M elements
+__global__ void __launch_bounds__(256) k_topk_hist3(TP p, int64_t ntiles) {
+  extern __shared__ uint32_t pre[];  // [ntiles + 1]
   __shared__ uint32_t h3[512];
+  __shared__ uint32_t s_b2, s_krem;
   for (int i = threadIdx.x; i < 512; i += blockDim.x) h3[i] = 0;
+  for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) pre[t] = p.w.segcnt[t];
+  select_bin(p.w.hist + 2048, 2048, p.w.ctl[CTL_KREM1], &s_b2, &s_krem);  // (ends in a barrier)
   __syncthreads();
-  const uint32_t M = p.w.ctl[CTL_M];
-  const uint32_t hi = (p.w.ctl[CTL_B1] << 11) | p.w.ctl[CTL_B2];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t key = p.w.keys[p.w.list[i]] & 0x7fffffffu;
+  // exclusive scan in place: thread t owns a run of `per` consecutive tiles
+  const int64_t per = cdiv(ntiles, 256);
+  const int64_t t0 = threadIdx.x * per, t1 = imin(ntiles, t0 + per);
+  uint64_t own = 0;
+  for (int64_t t = t0; t < t1; ++t) own += pre[t];
+  uint64_t total;
+  uint64_t run = block_exscan(own, &total);  // (barriers: every thread has read its run)
+  for (int64_t t = t0; t < t1; ++t) { const uint32_t c = pre[t]; pre[t] = (uint32_t)run; run += c; }
+  if (threadIdx.x == 0) pre[ntiles] = (uint32_t)total;
+  __syncthreads();
+  const uint32_t M = (uint32_t)total;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.w.ctl[CTL_M] = M;  // list length
+    p.w.ctl[CTL_B2] = s_b2;
+    p.w.ctl[CTL_KREM2] = s_krem;
+  }
+  const uint32_t hi = (p.w.ctl[CTL_B1] << 11) | s_b2;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+    int64_t lo = 0, up = ntiles;  // largest t with pre[t] <= j
+    while (up - lo > 1) {
+      const int64_t mid = (lo + up) >> 1;
+      if (pre[mid] <= j) lo = mid; else up = mid;
+    }
+    const uint32_t e = p.w.list[lo * CB + (j - pre[lo])];
+    p.w.list2[j] = e;
+    const uint32_t key = key_at(p, e) & 0x7fffffffu;
     if ((key >> 9) == hi) atomicAdd(&h3[key & 0x1ffu], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 512; i += blockDim.x)
     if (h3[i]) atomicAdd(&p.w.hist[4096 + i], h3[i]);
-}
-
-__global__ void k_topk_select3(TP p) {
-  __shared__ uint32_t b3, need;
-  select_bin(p.w.hist + 4096, 512, p.w.ctl[CTL_KREM2], &b3, &need);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    p.w.ctl[CTL_T] = (p.w.ctl[CTL_B1] << 20) | (p.w.ctl[CTL_B2] << 9) | b3;
-    p.w.ctl[CTL_NEED] = need;
+  if (last_cta(&p.w.ctl[CTL_DONE3])) {
+    __shared__ uint32_t s_b3, s_need;
+    select_bin(p.w.hist + 4096, 512, p.w.ctl[CTL_KREM2], &s_b3, &s_need);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      p.w.ctl[CTL_T] = (p.w.ctl[CTL_B1] << 20) | (p.w.ctl[CTL_B2] << 9) | s_b3;
+      p.w.ctl[CTL_NEED] = s_need;
+    }
   }
 }
 
@@ -393,9 +491,9 @@ __global__ void __launch_bounds__(256) k_topk_final(TP p) {
         const int64_t li = c0 + 128 * i + 4 * lane + q;
         ent[i][q] = 0;
         if (li < M) {
-          const uint32_t e = p.w.list[li];
+          const uint32_t e = p.w.list2[li];
           ent[i][q] = e;
-          const uint32_t key = p.w.keys[e] & 0x7fffffffu;
+          const uint32_t key = key_at(p, e) & 0x7fffffffu;
           gt |= (uint32_t)(key > T) << (4 * i + q);
           tie |= (uint32_t)(key == T) << (4 * i + q);
         }
@@ -428,7 +526,7 @@ __global__ void __launch_bounds__(256) k_topk_final(TP p) {
         if (is_gt || (is_tie && tie_b < need)) {
           const uint64_t slot = gt_b + (tie_b < need ? tie_b : need);
           const uint32_t e = ent[i][q];
-          const float c32 = __uint_as_float(p.w.keys[e]);
+          const float c32 = __uint_as_float(key_at(p, e));
           p.idx_out[slot] = e;
           p.val_out[slot] = c32;
           if (p.pro.r) p.pro.r[e] = __dsub_rn(p.pro.r[e], (double)c32);  // r = c - decode  (:412)
@@ -1253,21 +1351,34 @@ int encode_topk(const EncodeArgs& a, float* out) {
   p.vec = ((uintptr_t)p.pro.g % 16 == 0) && (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) &&
           (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0) && ((uintptr_t)out % 16 == 0);
   p.payload = a.payload;
+  // c32 after pass 1: f32(r) under EF, else the updated momentum, else the gradient — unless
+  // the fused output (zeroed by pass 1) aliases that gradient: then keys are materialised
+  if (p.pro.r) p.ksrc = KS_R;
+  else if (p.pro.m) { p.ksrc = KS_F; p.kf = p.pro.m; }
+  else if (out != p.pro.g) { p.ksrc = KS_F; p.kf = p.pro.g; }
+  else p.ksrc = KS_KEYS;
   p.hdr.algorithm = (uint32_t)a.spec->algorithm;
   p.hdr.original_len = (uint64_t)n;
   p.hdr.n_idx = p.hdr.n_val = p.hdr.cap = (uint32_t)k;
   cudaStream_t st = a.ctx.stream;
   const int64_t ntiles = cdiv(n, CB);
+  if (ntiles > H3_MAX_TILES) {
+    set_error("top-k group of %lld elements exceeds the supported %lld", (long long)n, (long long)(H3_MAX_TILES * CB));
+    return MC_EINVAL;
+  }
   // zero histograms + ctl + ticket + status in one memset (contiguous in the carve)
   const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (ntiles + 1);
   MC_API_CHECK(cudaMemsetAsync(p.w.hist, 0, zbytes, st));
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 1024), (int64_t)sm_count() * 8));
   note_launch(); k_topk_pass1<<<g1, 256, 0, st>>>(p);
-  note_launch(); k_topk_select1<<<1, 1024, 0, st>>>(p);
-  note_launch(); k_topk_pass2<<<(unsigned)imax(1, imin(ntiles, (int64_t)sm_count() * 4)), 256, 0, st>>>(p, ntiles);
-  note_launch(); k_topk_select2<<<1, 1024, 0, st>>>(p);
-  note_launch(); k_topk_hist3<<<(unsigned)sm_count(), 256, 0, st>>>(p);
-  note_launch(); k_topk_select3<<<1, 1024, 0, st>>>(p);
+  note_launch(); k_topk_pass2<<<(unsigned)ntiles, 256, 0, st>>>(p);
+  const int h3smem = (int)(4 * (ntiles + 1));
+  static int h3_cfg = 48 * 1024;  // dynamic smem limit set so far (benign race: idempotent growth)
+  if (h3smem > h3_cfg) {
+    MC_API_CHECK(cudaFuncSetAttribute(k_topk_hist3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (int)(H3_MAX_TILES + 1)));
+    h3_cfg = 4 * (int)(H3_MAX_TILES + 1);
+  }
+  note_launch(); k_topk_hist3<<<(unsigned)sm_count() * 2, 256, h3smem, st>>>(p, ntiles);
   // reset ticket + status for the final look-back pass (list length <= n)
   const int64_t ftiles = cdiv(n, CB_F);
   MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (ftiles + 1), st));
