@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--boundaries", default=None, help="comma separated cut list instead of the search")
     ap.add_argument("--search-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="elements per pipelined H2D/encode/D2H chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU oracle sample budget")
     ap.add_argument("--json-out", default=None)
@@ -341,16 +342,16 @@ def main():
     # ---- end to end through the public API: pinned host gradients in, averaged gradients out
     out_host = torch.empty(D, dtype=torch.float32).pin_memory()
     for _ in range(2):
-        sync.sync_host(host_grads, out_host)
+        sync.sync_host(host_grads, out_host, chunk_elems=args.e2e_chunk)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(sync.stream)
+    e0.record()  # every sync_host stream waits on the current stream, so this precedes all copies
     for _ in range(args.e2e_steps):
-        sync.sync_host(host_grads, out_host)
-    e1.record(sync.stream)
+        sync.sync_host(host_grads, out_host, chunk_elems=args.e2e_chunk)
+    e1.record()  # sync_host leaves the current stream waiting on its D2H and encode streams
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:

@@ -143,6 +143,23 @@ int mc_unpack(const float* fused, float* const* dsts, const int64_t* numels, int
 int mc_serialize(const mc_spec* spec, const void* payload, int64_t n, void* out, int64_t out_cap,
                  int64_t* out_len, void* stream);
 
+/* Host-buffer sync of one rank (world size 1), enqueued natively: the trainer's step on a
+ * worker's host gradient (trainer.py:360-395, one worker).  For each group: H2D of
+ * host_in[0, n) into dev (device slice of the flat gradient), the fused encode + single-
+ * rank aggregate in place, D2H into host_out — chunked on three streams (h2d / encode /
+ * d2h) so PCIe runs full duplex; chunk c of a call waits for the previous call's read-out
+ * of the same device chunk.  Chunk-wise encode for identity / fp16 / efsignsgd / onebit /
+ * int8, whole-group encode between the chunked copies otherwise.  mc_pipe_finish makes
+ * `s_wait` wait for the whole call.  The pipe owns only CUDA events (no device memory). */
+typedef struct mc_pipe mc_pipe;
+int mc_pipe_create(mc_pipe** out);
+void mc_pipe_destroy(mc_pipe* pipe);
+int mc_pipe_group(mc_pipe* pipe, const mc_spec* spec, const float* host_in, float* host_out, float* dev,
+                  int64_t n, int64_t chunk, double* residual, float* momentum, uint64_t key_lo, uint64_t key_hi,
+                  void* payload, void* workspace, int64_t workspace_bytes, uint32_t* err_flags, void* s_h2d,
+                  void* s_enc, void* s_d2h);
+int mc_pipe_finish(mc_pipe* pipe, void* s_enc, void* s_d2h, void* s_wait);
+
 #ifdef __cplusplus
 }
 #endif

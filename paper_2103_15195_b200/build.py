@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libmergecomp.so"
-SOURCES = ["mc_capi.cu", "mc_bucket.cu", "mc_dense.cu", "mc_sparse.cu", "mc_sign.cu"]
+SOURCES = ["mc_capi.cu", "mc_bucket.cu", "mc_dense.cu", "mc_sparse.cu", "mc_sign.cu", "mc_pipe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2", f"-I{ROOT / 'include'}"]
 

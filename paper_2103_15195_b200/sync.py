@@ -208,71 +208,65 @@ class GradSync:
             self.probe[1].append(ev)
         return x
 
-    CHUNKABLE = frozenset({"identity", "fp16", "efsignsgd", "onebit", "int8"})
-
     def sync_host(self, host_in: torch.Tensor, host_out: Optional[torch.Tensor] = None,
                   chunk_elems: int = 1 << 21) -> torch.Tensor:
         """The host-buffer entry point: copy a (pinned) host gradient buffer in, run one
         sync step, copy the averaged gradients back out — all stream-ordered.  On one
-        rank with a chunkable codec the copies are pipelined with the fused encode:
-        H2D of chunk c+1, encode+decode of chunk c and D2H of chunk c-1 overlap on three
-        streams (PCIe is full duplex)."""
+        rank the whole step is enqueued natively (mc_pipe_group): chunked H2D / fused
+        encode+aggregate / D2H on three streams, PCIe full duplex, and consecutive calls
+        overlap (a chunk is overwritten only after its previous read-out)."""
         if host_out is None:
             host_out = torch.empty(self.flat.numel(), dtype=torch.float32, pin_memory=True)
-        if self.world == 1 and self.fuse_local and self.spec.algorithm in self.CHUNKABLE and chunk_elems > 0:
-            return self._sync_host_pipelined(host_in, host_out, chunk_elems)
+        if self.world == 1 and self.fuse_local and chunk_elems > 0:
+            return self._sync_host_native(host_in, host_out, chunk_elems)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
             self.flat.copy_(host_in, non_blocking=True)
         self.step()
         with torch.cuda.stream(self.stream):
             host_out.copy_(self.flat, non_blocking=True)
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)  # host_out is ready in stream order
         return host_out
 
-    def _sync_host_pipelined(self, host_in, host_out, chunk_elems):
+    def _sync_host_native(self, host_in, host_out, chunk_elems):
         import ctypes
-        import math
 
         from .compressors import _WS, _stream_ptr
 
-        if not hasattr(self, "_h2d"):
+        lib = _native.lib()
+        if getattr(self, "_pipe", None) is None:
+            h = ctypes.c_void_p()
+            _native.check(lib.mc_pipe_create(ctypes.byref(h)), "mc_pipe_create")
+            self._pipe = h
             self._h2d = torch.cuda.Stream(device=self.device)
             self._d2h = torch.cuda.Stream(device=self.device)
+        if not (host_in.is_pinned() and host_out.is_pinned()):
+            raise ValueError("sync_host needs pinned host buffers")
         cur = torch.cuda.current_stream(self.device)
         for st in (self._h2d, self.stream, self._d2h):
             st.wait_stream(cur)
-        align = math.lcm(int(self.spec.bucket_size), 32) if self.spec.algorithm not in ("identity", "fp16") else 32
-        chunk = max(align, chunk_elems // align * align)
-        lib = _native.lib()
         plan = self._plan(self.partition)
+        sh, se, sd = _stream_ptr(self._h2d), _stream_ptr(self.stream), _stream_ptr(self._d2h)
         for g, grp in enumerate(plan):
             lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
-            base = self.flat[grp.start:grp.end]
             ws = _WS.get(self.device, _native.workspace_bytes(self.cspec, grp.n))
-            for begin in range(0, grp.n, chunk):
-                cnt = min(chunk, grp.n - begin)
-                a = grp.start + begin
-                with torch.cuda.stream(self._h2d):
-                    self.flat[a:a + cnt].copy_(host_in[a:a + cnt], non_blocking=True)
-                    ev_in = torch.cuda.Event()
-                    ev_in.record(self._h2d)
-                self.stream.wait_event(ev_in)
-                _native.check(lib.mc_encode_range(
-                    ctypes.byref(self.cspec), base.data_ptr(), grp.n, begin, cnt,
-                    None if grp.residual is None else grp.residual.data_ptr(),
-                    None if grp.momentum is None else grp.momentum.data_ptr(), lo, hi, grp.payload.data_ptr(),
-                    ws.data_ptr(), ws.numel(), base.data_ptr(), self.err.data_ptr(), _stream_ptr(self.stream)),
-                    "mc_encode_range")
-                ev_c = torch.cuda.Event()
-                ev_c.record(self.stream)
-                self._d2h.wait_event(ev_c)
-                with torch.cuda.stream(self._d2h):
-                    host_out[a:a + cnt].copy_(self.flat[a:a + cnt], non_blocking=True)
-        cur.wait_stream(self._d2h)
-        cur.wait_stream(self.stream)
-        self.stream.wait_stream(self._d2h)  # later steps must not overwrite flat before it is read out
+            _native.check(lib.mc_pipe_group(
+                self._pipe, ctypes.byref(self.cspec), host_in.data_ptr() + 4 * grp.start,
+                host_out.data_ptr() + 4 * grp.start, self.flat.data_ptr() + 4 * grp.start, grp.n, chunk_elems,
+                None if grp.residual is None else grp.residual.data_ptr(),
+                None if grp.momentum is None else grp.momentum.data_ptr(), lo, hi, grp.payload.data_ptr(),
+                ws.data_ptr(), ws.numel(), self.err.data_ptr(), sh, se, sd), "mc_pipe_group")
+        _native.check(lib.mc_pipe_finish(self._pipe, se, sd, _stream_ptr(cur)), "mc_pipe_finish")
         self.iteration += 1
         return host_out
+
+    def __del__(self):
+        pipe = getattr(self, "_pipe", None)
+        if pipe is not None:
+            try:
+                _native.lib().mc_pipe_destroy(pipe)
+            except Exception:
+                pass
 
     # ------------------------------------------------------------ overlap with backward (WFBP)
     def attach(self, params_backprop_order: Sequence[torch.nn.Parameter]) -> None:

@@ -113,7 +113,8 @@ def test_large_group_against_oracle():
             assert np.array_equal(_bits(st_d.residual.cpu().numpy()), _bits(st_o.residual)), algo
 
 
-@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8", "fp16", "identity", "qsgd", "dgc_lite"])
+@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8", "fp16", "identity", "qsgd", "dgc_lite", "topk",
+                                  "terngrad", "signsgd", "signum", "randk", "threshold"])
 def test_sync_host_pipelined_equals_device_step(algo):
     """GradSync.sync_host (chunked H2D / fused encode / D2H pipeline) == device step()."""
     from paper_2103_15195_b200 import gradsets
@@ -179,3 +180,28 @@ def test_backward_overlap_hooks_equal_post_backward_step(algo):
         assert torch.equal(s1.flat.view(torch.int32), s2.flat.view(torch.int32)), (algo, it)
         assert all(g1.data_ptr() == s1.flat[a:a + 1].data_ptr() for g1, a in zip([p.grad for p in p1], prof.offsets()[:-1]))
     s1.detach()
+
+
+@pytest.mark.parametrize("algo", ["efsignsgd", "dgc_lite"])
+def test_sync_host_back_to_back_calls(algo):
+    """Consecutive native host syncs enqueued without a host synchronisation in between
+    (each call's H2D chases the previous call's read-out chunk by chunk) give the same
+    outputs as synchronised device steps."""
+    from paper_2103_15195_b200 import gradsets
+    from paper_2103_15195_b200.spec import CompressorSpec
+    from paper_2103_15195_b200.sync import GradSync
+
+    spec = CompressorSpec(algo, sparsity=0.999)
+    prof = gradsets.profile("resnet50_161")
+    a = GradSync(spec, prof, root_seed=3)
+    b = GradSync(spec, prof, root_seed=3)
+    ins = [torch.from_numpy(gradsets.synthetic_gradients("resnet50_161", it, 0)).pin_memory() for it in range(3)]
+    outs = [torch.empty_like(x).pin_memory() for x in ins]
+    for x, o in zip(ins, outs):
+        a.sync_host(x, o, chunk_elems=1 << 19)
+    torch.cuda.synchronize()
+    for x, o in zip(ins, outs):
+        b.flat.copy_(x)
+        b.step()
+        torch.cuda.synchronize()
+        assert torch.equal(o.view(torch.int32), b.flat.cpu().view(torch.int32))
