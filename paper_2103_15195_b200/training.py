@@ -16,6 +16,7 @@ from typing import Callable, Optional, Sequence
 
 import torch
 
+from .costmodel import CostParams, fit_params, microbench
 from .profiles import LayerProfile, ModelProfile, Partition
 from .spec import CompressorSpec
 from .sync import GradSync
@@ -72,3 +73,65 @@ class OverlapHandle:
             ms = float(t.item())
         self.sync.pin_partition(prev)
         return ms
+
+    # ---- analytic search inputs: measured backprop profile + fitted costs
+    def measure_profile(self, repetitions: int = 5) -> ModelProfile:
+        """Per-tensor backward compute times on this GPU: a CUDA event is recorded on the
+        backward stream when each gradient is accumulated (the same hook point that
+        launches a group's sync) and the median gap to the previous one is the tensor's
+        compute_time (ms).  Syncs are not armed while measuring."""
+        events = {}
+
+        def mk(i):
+            def hook(_p):
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                events[i] = ev
+            return hook
+
+        hooks = [p.register_post_accumulate_grad_hook(mk(i)) for i, p in enumerate(self.params)]
+        per = [[] for _ in self.params]
+        try:
+            for rep in range(repetitions + 1):
+                self.sync.flat.zero_()
+                loss = self.loss_fn(self.model)
+                start = torch.cuda.Event(enable_timing=True)
+                start.record()
+                events.clear()
+                loss.backward()
+                torch.cuda.synchronize()
+                if rep == 0:
+                    continue  # warm-up
+                prev = start
+                for i in range(len(self.params)):  # backprop order = readiness order
+                    ev = events.get(i)
+                    if ev is None:
+                        per[i].append(0.0)
+                        continue
+                    per[i].append(max(prev.elapsed_time(ev), 0.0))
+                    prev = ev
+        finally:
+            for h in hooks:
+                h.remove()
+        import statistics
+
+        times = [statistics.median(v) for v in per]
+        return ModelProfile(type(self.model).__name__,
+                            tuple(LayerProfile(i, p.numel(), t) for i, (p, t) in enumerate(zip(self.params, times))))
+
+    def fit_costs(self, profile: Optional[ModelProfile] = None, sizes: Optional[Sequence[int]] = None,
+                  repetitions: int = 10) -> CostParams:
+        """CostParams from device samples: h from microbench on this GPU; g from the NCCL
+        allgather of real payloads when there is more than one rank (else 0); A = the
+        measured backprop time."""
+        prof = profile or self.measure_profile()
+        total = prof.total_size
+        if sizes is None:
+            sizes = sorted({max(1024, int(total * f)) for f in (0.01, 0.05, 0.1, 0.25, 0.5, 1.0)})
+        h = microbench(self.sync.spec, sizes, repetitions, device=self.sync.device)
+        g = ()
+        if self.sync.world > 1:
+            from .costmodel import comm_microbench
+
+            g = comm_microbench(self.sync.spec, sizes, repetitions, group=self.sync.pg, device=self.sync.device)
+        return fit_params(h, g, A=prof.total_compute)

@@ -56,6 +56,22 @@ def main():
     res["searched"] = {"boundaries": list(search.partition.boundaries), "F_ms": search.F_ms,
                        "evaluations": search.evaluations, "termination": search.termination}
     res["searched_ms"] = med(search.partition)
+    # analytic search: measured backprop profile + device-fitted costs,
+    # Algorithm 2 on the iteration-time model, no timed iterations per candidate
+    import time as _time
+
+    from paper_2103_15195_b200 import simulator as SIM
+    from paper_2103_15195_b200.scheduler import analytic_evaluator, heuristic_search
+
+    t0 = _time.perf_counter()
+    prof = h.measure_profile(repetitions=5)
+    costs = h.fit_costs(prof, repetitions=10)
+    cfg = SIM.SimConfig(prof, Partition.merged(n), spec, costs)
+    ares = heuristic_search(SearchConfig(Y=2, alpha=0.02, evaluator=analytic_evaluator(cfg)), prof)
+    res["analytic"] = {"costs": costs.to_dict(), "boundaries": list(ares.partition.boundaries),
+                       "predicted_F_ms": ares.F_ms, "evaluations": ares.evaluations,
+                       "predicted_merged_ms": SIM.objective_F(cfg), "search_wall_s": _time.perf_counter() - t0,
+                       "measured_ms": med(ares.partition)}
     fwd_bwd = []
     for _ in range(a.reps):  # compute-only reference: forward + backward, no sync
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
