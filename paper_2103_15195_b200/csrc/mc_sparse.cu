@@ -918,14 +918,24 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
                                uint8_t* tables) {
   extern __shared__ uint32_t masks[];  // [DW + RX][32]
   __shared__ int64_t s_L;
+  __shared__ double s_part[32];
   const int64_t w = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    double e = 0.0;  // expected offset at the window start (sum of earlier windows)
-    for (int64_t i = 0; i < w; ++i) e += expw[i];
-    const int64_t L = imax(0, (int64_t)floor(e) - DW / 2);
-    s_L = L;
-    Lw[w] = L;
+  {  // expected offset at the window start: sum of the earlier windows' expectations
+     // (block reduction; the value only centres the speculated range — the chain checks it)
+    double e = 0.0;
+    for (int64_t i = tid; i < w; i += blockDim.x) e += expw[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+    if (lane == 0) s_part[warp] = e;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s_part[i];
+      const int64_t L = imax(0, (int64_t)floor(t) - DW / 2);
+      s_L = L;
+      Lw[w] = L;
+    }
   }
   __syncthreads();
   const int64_t L = s_L;

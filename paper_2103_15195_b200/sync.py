@@ -164,6 +164,38 @@ class GradSync:
                            cspec=self.cspec)
         return 0
 
+    # ------------------------------------------------------------ CUDA Graph of a pinned partition
+    GRAPHABLE = frozenset({"identity", "fp16", "efsignsgd", "onebit", "int8", "signsgd", "signum", "topk",
+                           "dgc_lite", "threshold"})
+
+    def capture_graph(self, partition: Optional[Partition] = None) -> None:
+        """Record one rank's whole sync step for ``partition`` (default: the pinned one) as a
+        CUDA Graph; ``step()`` then replays it with one launch instead of one ctypes call
+        and 1-5 kernel launches per group (the launch-bound many-small-groups case of
+        SURVEY.md §8(f)-4).  One rank and deterministic codecs only: the stochastic
+        codecs' Philox keys change every iteration and are kernel arguments.  Capturing
+        runs nothing; gradients and codec state are untouched."""
+        if self.world != 1 or not self.fuse_local:
+            raise ValueError("capture_graph: single-rank fused sync only")
+        if self.spec.algorithm not in self.GRAPHABLE:
+            raise ValueError(f"capture_graph: {self.spec.algorithm} draws per-iteration Philox keys")
+        from .compressors import _WS
+
+        part = self.partition if partition is None else self._resolve(partition)
+        self.partition = part
+        plan = self._plan(part)
+        need = max(_native.workspace_bytes(self.cspec, grp.n) for grp in plan)
+        ws = _WS.get(self.device, need)  # sized before capture: the graph keeps these pointers
+        graph = torch.cuda.CUDAGraph()
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.graph(graph, stream=self.stream):
+            for g, grp in enumerate(plan):
+                self._sync_group(g, grp)
+        self._graph = (part.boundaries, graph, ws, len(plan))
+
+    def drop_graph(self) -> None:
+        self._graph = None
+
     def step(self, partition: Optional[Partition] = None) -> None:
         """One synchronisation of every group of ``partition`` (default: the pinned one),
         enqueued on the side stream after the gradients' producer stream.
@@ -173,6 +205,14 @@ class GradSync:
         their own gather only — encode(g+1) runs while allgather(g) is on NVLink (the
         compute and communication channels of MergeComp, simulator.py:114-142)."""
         part = self.partition if partition is None else self._resolve(partition)
+        graph = getattr(self, "_graph", None)
+        if graph is not None and graph[0] == part.boundaries:
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(self.stream):
+                graph[1].replay()
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
+            self.iteration += 1
+            return
         plan = self._plan(part)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
