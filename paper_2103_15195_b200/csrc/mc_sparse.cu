@@ -914,9 +914,11 @@ __global__ void k_randk_expect(RP p, double* expw, int64_t nwin) {
   }
 }
 
+constexpr int HQ = 16;  // queued filter hits per thread (mean ~3.2 at 1% density)
 __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, const double* expw, int64_t* Lw,
                                uint8_t* tables) {
-  extern __shared__ uint32_t masks[];  // [DW + RX][32]
+  extern __shared__ uint32_t masks[];  // [DW + RX][32] then the hit queues [1024][HQ] u16
+  uint16_t* hitq = reinterpret_cast<uint16_t*>(masks + (DW + RX) * 32);
   __shared__ int64_t s_L;
   __shared__ double s_part[32];
   const int64_t w = blockIdx.x;
@@ -942,28 +944,35 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
   const Philox ph{p.k0, p.k1};
   const int64_t pos = w * WP + tid;
   const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
-  // candidate c serves step s = pos - L - c; lo32(w * excl) moves by -+w per candidate, so the
-  // "may reject" filter (left < excl) is two integer ops; exact thresholds only for hits
+  for (int i = tid; i < (DW + RX) * 32; i += blockDim.x) masks[i] = 0u;
+  __syncthreads();
+  // candidate c serves step s = pos - L - c: lo32(w * excl) moves by -+w and excl by -+1 per
+  // candidate, so the "may reject" filter (left < excl, p ~ excl / 2^32 < 1%) is two adds and a
+  // compare; the few hits take the exact threshold test and set their bit in the shared
+  // [candidate][warp] mask matrix
   const int64_t s0 = pos - L;
   const uint32_t ex0 = excl_of(p, s0);
-  const uint32_t l0 = w32 * ex0;
+  uint32_t left = w32 * ex0, ex = ex0;
   const uint32_t dl = p.tail_shuffle ? w32 : (0u - w32);
-  for (int c0 = 0; c0 < DW + RX; c0 += 32) {
-    uint32_t hit = 0;
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const uint32_t ex = p.tail_shuffle ? ex0 + (uint32_t)(c0 + c) : ex0 - (uint32_t)(c0 + c);
-      hit |= (uint32_t)((l0 + (uint32_t)(c0 + c) * dl) < ex) << c;
+  const uint32_t de = p.tail_shuffle ? 1u : 0xffffffffu;
+  // hits are queued per thread and tested after the scan, all lanes together: testing them
+  // inside the scan made every warp run the exact test (an integer modulo) whenever any of
+  // its 32 lanes hit (~17% of candidates), not ~0.6%
+  uint16_t* q = hitq + tid * HQ;
+  int nh = 0;
+#pragma unroll 8
+  for (int c = 0; c < DW + RX; ++c) {
+    if (left < ex) {
+      if (nh < HQ) q[nh++] = (uint16_t)c;
+      else if (rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);  // (never in practice)
     }
-    for (uint32_t h = hit; h; h &= h - 1) {
-      const int c = __ffs(h) - 1;
-      if (!rejects(p, w32, s0 - (c0 + c))) hit &= ~(1u << c);
-    }
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const unsigned m = __ballot_sync(FULL, (hit >> c) & 1u);
-      if (lane == 0) masks[(c0 + c) * 32 + warp] = m;
-    }
+    left += dl;
+    ex += de;
+  }
+  const int nmax = __reduce_max_sync(FULL, nh);
+  for (int i = 0; i < nmax; ++i) {
+    const int c = i < nh ? q[i] : 0;
+    if (i < nh && rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);
   }
   __syncthreads();
   if (tid < DW) {  // walk entering with offset L + tid
@@ -980,45 +989,73 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
   }
 }
 
+// chain, in two levels: windows are grouped by CG; k_randk_compose turns each group's CG
+// tables into one composed table over the group's first window (thread e walks the
+// group from entering offset L + e), then k_randk_chain runs the serial recurrence over
+// groups (nwin / CG dependent lookups instead of nwin) and replays every group's windows
+// from its exact entering offset in parallel, writing tin[w].
+constexpr int CG = 16;
+__global__ void __launch_bounds__(DW) k_randk_compose(const int64_t* Lw, const uint8_t* tables, int64_t nwin,
+                                                      int* comp) {
+  const int64_t g = blockIdx.x, w0 = g * CG;
+  int t = (int)Lw[w0] + (int)threadIdx.x;
+  for (int64_t w = w0; w < imin(nwin, w0 + CG); ++w) {
+    const unsigned c = (unsigned)(t - (int)Lw[w]);
+    const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
+    if (r == 255) { t = -1; break; }  // leaves the speculated range inside the group
+    t += r;
+  }
+  comp[g * DW + threadIdx.x] = t;
+}
+
 __global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, const uint8_t* tables, int64_t nwin,
-                                                      int64_t* tin, WalkCtl* ctl) {
-  extern __shared__ uint8_t srow[];  // [CH][DW]
-  constexpr int CH = 96;
-  __shared__ int64_t s_L[CH];
-  __shared__ int64_t s_t;
-  __shared__ int s_stop;
-  if (threadIdx.x == 0) { s_t = 0; s_stop = 0; ctl->fail_base = -1; ctl->nwin_used = nwin; }
-  __syncthreads();
-  for (int64_t w0 = 0; w0 < nwin && !s_stop; w0 += CH) {
-    const int cnt = (int)imin(CH, nwin - w0);
-    const uint4* src = reinterpret_cast<const uint4*>(tables + w0 * DW);
-    for (int i = threadIdx.x; i < cnt * DW / 16; i += blockDim.x) reinterpret_cast<uint4*>(srow)[i] = src[i];
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) s_L[i] = Lw[w0 + i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t t = s_t;
-      for (int i = 0; i < cnt; ++i) {
-        const int64_t w = w0 + i;
-        if (w * WP - t >= p.k) { ctl->nwin_used = w; s_stop = 1; break; }  // every step served
-        const int64_t c = t - s_L[i];
-        const uint8_t r = (c >= 0 && c < DW) ? srow[i * DW + c] : (uint8_t)255;
-        if (r == 255) {  // outside the speculated range: hand over to the serial walker
-          ctl->fail_base = w * WP;
-          ctl->fail_t0 = t;
-          ctl->nwin_used = w;
-          s_stop = 1;
-          break;
-        }
-        tin[w] = t;
-        t += r;
-      }
-      s_t = t;
-      if (!s_stop && w0 + cnt >= nwin && nwin * WP - t < p.k) {  // ran out of windows
-        ctl->fail_base = nwin * WP;
-        ctl->fail_t0 = t;
-      }
+                                                      const int* comp, int* tg, int64_t* tin, WalkCtl* ctl) {
+  __shared__ int s_ng, s_fail_g;
+  __shared__ unsigned long long s_used;
+  const int64_t ngrp = cdiv(nwin, CG);
+  if (threadIdx.x == 0) {
+    ctl->fail_base = -1;
+    int t = 0;
+    int64_t g = 0;
+    int fail_g = -1;
+    for (; g < ngrp; ++g) {
+      tg[g] = t;
+      const unsigned c = (unsigned)(t - (int)Lw[g * CG]);
+      const int nt = c < (unsigned)DW ? comp[g * DW + c] : -1;
+      if (nt < 0) { fail_g = (int)g; ++g; break; }  // resolve inside this group below
+      t = nt;
     }
-    __syncthreads();
+    s_ng = (int)g;  // groups with a known entering offset
+    s_fail_g = fail_g;
+    s_used = (unsigned long long)nwin;
+  }
+  __syncthreads();
+  // replay each group's windows from its entering offset: tin, the first window whose steps
+  // are all served (nwin_used) and, for the failing group, the hand-over to the serial walker
+  for (int64_t g = threadIdx.x; g < s_ng; g += blockDim.x) {
+    int t = tg[g];
+    for (int64_t w = g * CG; w < imin(nwin, (g + 1) * CG); ++w) {
+      if (w * WP - (int64_t)t >= p.k) { atomicMin(&s_used, (unsigned long long)w); break; }
+      const unsigned c = (unsigned)(t - (int)Lw[w]);
+      const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
+      if (r == 255) {  // only in the failing group: the serial walker continues from here
+        atomicMin(&s_used, (unsigned long long)w);
+        ctl->fail_base = w * WP;
+        ctl->fail_t0 = t;
+        break;
+      }
+      tin[w] = t;
+      t += r;
+    }
+    if (g == s_ng - 1 && s_fail_g < 0 && (g + 1) * CG >= nwin && nwin * WP - (int64_t)t < p.k) {
+      ctl->fail_base = nwin * WP;  // ran out of windows before every step was served
+      ctl->fail_t0 = t;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->nwin_used = (int64_t)s_used;
+    if (ctl->fail_base >= 0 && ctl->fail_base / WP > (int64_t)s_used) ctl->fail_base = -1;  // served before
   }
 }
 
@@ -1475,13 +1512,14 @@ int encode_randk(const EncodeArgs& a, float* out) {
     int64_t* tin = reinterpret_cast<int64_t*>(wsb + 2 * a16(8 * nwin));
     WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + 3 * a16(8 * nwin));
     uint8_t* tables = wsb + 3 * a16(8 * nwin) + 64;
+    int* comp = reinterpret_cast<int*>(tables + a16(nwin * DW));           // [ngroups][DW]
+    int* tg = comp + cdiv(nwin, CG) * DW;                                    // [ngroups]
     note_launch(); k_randk_words<<<(unsigned)imax(1, imin(cdiv(nwords, 8 * 256), (int64_t)sm_count() * 4)), 256, 0, st>>>(p, p.w.list, nwords);
-    if (4 * n >= a16(4 * nwords) + 3 * a16(8 * nwin) + 64 + nwin * DW) {  // room for the parallel walk
+    if (4 * n >= a16(4 * nwords) + 3 * a16(8 * nwin) + 64 + a16(nwin * DW) + 4 * (cdiv(nwin, CG) * (DW + 1))) {  // room for the parallel walk
       static bool configured = false;
-      const int tsmem = (DW + RX) * 32 * 4;
+      const int tsmem = (DW + RX) * 32 * 4 + 1024 * HQ * 2;
       if (!configured) {
-        if (cudaFuncSetAttribute(k_randk_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem) != cudaSuccess ||
-            cudaFuncSetAttribute(k_randk_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * DW) != cudaSuccess) {
+        if (cudaFuncSetAttribute(k_randk_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem) != cudaSuccess) {
           set_error("randk walk smem configuration failed");
           return MC_ECUDA;
         }
@@ -1489,7 +1527,9 @@ int encode_randk(const EncodeArgs& a, float* out) {
       }
       note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
       note_launch(); k_randk_tables<<<(unsigned)nwin, 1024, tsmem, st>>>(p, p.w.list, nwords, expw, Lw, tables);
-      note_launch(); k_randk_chain<<<1, 1024, 96 * DW, st>>>(p, Lw, tables, nwin, tin, ctl);
+      const int64_t ngrp = cdiv(nwin, CG);
+      note_launch(); k_randk_compose<<<(unsigned)ngrp, DW, 0, st>>>(Lw, tables, nwin, comp);
+      note_launch(); k_randk_chain<<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, tg, tin, ctl);
       note_launch(); k_randk_emit_draws<<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);
       note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, &ctl->fail_base);
     } else {

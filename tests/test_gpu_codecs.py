@@ -125,3 +125,24 @@ def test_corrupt_indices_rejected(C):
 def test_derive_seed_native_matches_table(C):
     for root, w, t, g, lo, hi in G.store()["derive_seed.table"].tolist():
         assert C.derive_seed(root, w, t, g) == (lo | (hi << 64))
+
+
+@pytest.mark.parametrize("n,sparsity", [(2_000_003, 0.99), (3_000_000, 0.995), (1_500_000, 0.9)])
+def test_randk_multi_window_walk_matches_oracle(n, sparsity, C):
+    """randk at sizes where the draw walk spans many 1024-position windows (speculative
+    tables + chain + emit on many SMs; 0.9 takes numpy's tail-shuffle branch): indices and
+    values bit-exact against the oracle's Generator.choice restatement."""
+    import torch
+
+    import mergecomp_oracle as O
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    spec = CompressorSpec("randk", sparsity=sparsity)
+    rng = np.random.default_rng(n)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    seed = O.derive_seed(7, 0, 3, 1)
+    p_dev, _ = C.encode(spec, torch.from_numpy(g).cuda(), None, seed=seed)
+    p_ref, _ = O.encode(spec, g, None, seed=seed)
+    d = p_dev.to_host()
+    assert np.array_equal(np.asarray(d.indices), np.asarray(p_ref.indices))
+    assert np.array_equal(np.asarray(d.values).view(np.uint32), np.asarray(p_ref.values).view(np.uint32))
