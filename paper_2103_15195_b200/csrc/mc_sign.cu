@@ -12,13 +12,15 @@
 //   pass 2  one CTA combines the 2^(D-3) subtree sums as a perfect binary tree and
 //           writes the scaler f32(f64(0 + P) / n);
 //   pass 3  (error feedback only) r = c - (+-s).
+#include <cstdlib>
+
 #include "mc_internal.cuh"
 
 namespace mc {
 namespace {
 
 constexpr int SW = 8;  // warps (nodes) per CTA in pass 1
-constexpr int NODE_MAX = 1024;  // longest node the pass-1 kernels stage (8 chunks of 128)
+constexpr int NODE_MAX = 2048;  // longest node the pass-1 kernels stage (16 chunks of 128)
 
 struct SP {
   Prologue pro;
@@ -129,12 +131,18 @@ __device__ __forceinline__ float sign_node(const SP& p, int node, float* a) {
   }
   flag(p.err, nanacc != 0.0f, MC_ERR_NONFINITE);
   __syncwarp();
-  return warp_pairwise_small<3>([&](int q) { return a[spos(q)]; }, L);
+  // levels above the leaves (<= 128 elements): a split leaves children <= len/2 + 7.5, so
+  // after d splits a node is <= L/2^d + 15; depth 3 holds up to L = 904, 4 up to 1808
+  auto get = [&](int q) { return a[spos(q)]; };
+  if (NCH <= 4 || L <= 904) return warp_pairwise_small<3>(get, L);
+  if (NCH <= 8 || L <= 1808) return warp_pairwise_small<4>(get, L);
+  return warp_pairwise_small<5>(get, L);
 }
 
 template <int NCH, bool MOM, bool EF, bool VEC>
 __global__ void __launch_bounds__(SW * 32) k_sign_nodes(SP p) {
-  __shared__ __align__(16) float sm[SW][160 * NCH];
+  extern __shared__ __align__(16) float sm_dyn[];  // [SW][160 * NCH]
+  float(*sm)[160 * NCH] = reinterpret_cast<float(*)[160 * NCH]>(sm_dyn);
   __shared__ float s_node[SW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
@@ -151,9 +159,9 @@ __global__ void __launch_bounds__(SW * 32) k_sign_nodes(SP p) {
 // small trees (D < 3): one warp per node
 template <bool MOM, bool EF>
 __global__ void k_sign_nodes_small(SP p) {
-  __shared__ __align__(16) float sm[160 * 8];
+  __shared__ __align__(16) float sm[160 * 16];
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
-  const float s = sign_node<8, MOM, EF, false>(p, blockIdx.x, sm);
+  const float s = sign_node<16, MOM, EF, false>(p, blockIdx.x, sm);
   if (threadIdx.x == 0) p.partial[blockIdx.x] = s;
 }
 
@@ -165,12 +173,23 @@ void launch_nodes(const SP& p, int64_t n, int64_t nodes, cudaStream_t st) {
   if (p.D >= 3) {
     // longest node at depth D is < (n >> D) + 8 (each split leaves the right child <= len/2 + 8)
     const dim3 grid((unsigned)(nodes / SW));
-    if ((n >> p.D) + 16 <= 512) {
-      if (vec) k_sign_nodes<4, MOM, EF, true><<<grid, SW * 32, 0, st>>>(p);
-      else k_sign_nodes<4, MOM, EF, false><<<grid, SW * 32, 0, st>>>(p);
+    const int64_t longest = (n >> p.D) + 16;
+    constexpr int sm4 = SW * 160 * 4 * 4, sm8 = SW * 160 * 8 * 4, sm16 = SW * 160 * 16 * 4;
+    if (longest <= 512) {
+      if (vec) k_sign_nodes<4, MOM, EF, true><<<grid, SW * 32, sm4, st>>>(p);
+      else k_sign_nodes<4, MOM, EF, false><<<grid, SW * 32, sm4, st>>>(p);
+    } else if (longest <= 1024) {
+      if (vec) k_sign_nodes<8, MOM, EF, true><<<grid, SW * 32, sm8, st>>>(p);
+      else k_sign_nodes<8, MOM, EF, false><<<grid, SW * 32, sm8, st>>>(p);
     } else {
-      if (vec) k_sign_nodes<8, MOM, EF, true><<<grid, SW * 32, 0, st>>>(p);
-      else k_sign_nodes<8, MOM, EF, false><<<grid, SW * 32, 0, st>>>(p);
+      static bool cfg = false;  // idempotent (benign race)
+      if (!cfg) {
+        cudaFuncSetAttribute(k_sign_nodes<16, MOM, EF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
+        cudaFuncSetAttribute(k_sign_nodes<16, MOM, EF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
+        cfg = true;
+      }
+      if (vec) k_sign_nodes<16, MOM, EF, true><<<grid, SW * 32, sm16, st>>>(p);
+      else k_sign_nodes<16, MOM, EF, false><<<grid, SW * 32, sm16, st>>>(p);
     }
   } else {
     k_sign_nodes_small<MOM, EF><<<(unsigned)nodes, 32, 0, st>>>(p);
@@ -201,11 +220,16 @@ __global__ void k_sign_ef(SP p) {
   }
 }
 
+int sign_node_target() {
+  static const int v = [] { const char* e = getenv("MC_SIGN_NODE"); return e ? atoi(e) : 880; }();
+  return v;
+}
+
 int depth_for(int64_t n) {
   const int64_t P = n / 8;
   int D = 0;
   // every node at depth < D is split (length > 128); stop once nodes are <= ~800 elements
-  while (D < 18 && (P >> D) >= 17 && (n >> D) > 448) ++D;
+  while (D < 18 && (P >> D) >= 17 && (n >> D) > sign_node_target()) ++D;
   return D;
 }
 

@@ -146,3 +146,21 @@ def test_randk_multi_window_walk_matches_oracle(n, sparsity, C):
     d = p_dev.to_host()
     assert np.array_equal(np.asarray(d.indices), np.asarray(p_ref.indices))
     assert np.array_equal(np.asarray(d.values).view(np.uint32), np.asarray(p_ref.values).view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [25_557_032, 120_000_001])
+def test_signsgd_large_group_scale_matches_numpy(n, C):
+    """signsgd's scaler over a whole large group (numpy's float32 pairwise mean): node
+    trees of ~800 (depth-3 leaves) and ~920 elements (depth-4) — the scale bit-exact, and
+    the sign bits equal np.packbits(x >= 0)."""
+    import torch
+
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3)
+    p, _ = C.encode(CompressorSpec("signsgd"), torch.from_numpy(x).cuda(), None, seed=0)
+    h = p.to_host()
+    want = np.float32(np.abs(x).mean())
+    assert np.asarray(h.values).view(np.uint32)[0] == np.asarray([want]).view(np.uint32)[0]
+    assert np.array_equal(np.asarray(h.bits), np.packbits(x >= 0))
