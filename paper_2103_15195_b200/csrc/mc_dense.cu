@@ -303,6 +303,45 @@ __global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
   }
 }
 
+// One payload of a whole-group scale (signsgd / signum, world size 1): out = bit ? s : -s
+// (compressors.py:476-481, then aggregate's 0 + d / f32(1)).  A warp expands 1024
+// elements: lane l loads sign word l, and every store is one contiguous 512-byte row built
+// from the word of lane 4j + l/8 (a shuffle) — pure streaming writes.
+__global__ void __launch_bounds__(256) k_decode_sign_one(DP p) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(p.base);
+    if (h->algorithm != p.algo || h->original_len != (uint64_t)p.n || h->n_val != p.n_val || h->n_bits != p.n_bits)
+      atomicOr(p.err, MC_ERR_HEADER);
+  }
+  const float s = __fadd_rn(0.0f, reinterpret_cast<const float*>(p.base + p.off_val)[0]);
+  const float ns = __fadd_rn(0.0f, __fmul_rn(-1.0f, reinterpret_cast<const float*>(p.base + p.off_val)[0]));
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(p.base + p.off_bits);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwords = cdiv(p.n, 32);
+  const bool vout = ((uintptr_t)p.out % 16) == 0;
+  const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t wb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wb < nwords; wb += wstride) {
+    const uint32_t mine = wb + lane < nwords ? words[wb + lane] : 0u;
+    const int64_t e_base = 32 * wb;
+    const bool full = vout && e_base + 1024 <= p.n;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t wv = __shfl_sync(FULL, mine, 4 * j + (lane >> 3));
+      const int sh = 8 * ((lane >> 1) & 3) + ((lane & 1) ? 0 : 4);  // nibble of elements 4l..4l+3
+      const uint32_t nib = (wv >> sh) & 0xfu;
+      const float4 v = make_float4((nib & 8) ? s : ns, (nib & 4) ? s : ns, (nib & 2) ? s : ns, (nib & 1) ? s : ns);
+      const int64_t e0 = e_base + 128 * j + 4 * lane;
+      if (full) {
+        __stcs(reinterpret_cast<float4*>(p.out + e0), v);
+      } else {
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int q = 0; q < 4; ++q)
+          if (e0 + q < p.n) p.out[e0 + q] = vv[q];
+      }
+    }
+  }
+}
+
 template <int ALGO, bool SAMEB>
 __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
   if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
@@ -403,6 +442,13 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
   const int a = s->algorithm;
   const bool sign32 = (a == MC_SIGNSGD || a == MC_SIGNUM) ||
                       ((a == MC_EFSIGNSGD || a == MC_ONEBIT || (a == MC_QSGD && p.width == 8)) && p.B % 32 == 0);
+  if ((a == MC_SIGNSGD || a == MC_SIGNUM) && nranks == 1) {
+    const unsigned g1 = (unsigned)imax(1, imin(cdiv(cdiv(L.n, 32), 256), (int64_t)sm_count() * 8));
+    note_launch();
+    k_decode_sign_one<<<g1, 256, 0, st>>>(p);
+    MC_LAUNCH_CHECK();
+    return MC_OK;
+  }
   if (sign32) {
     const unsigned g32 = (unsigned)imax(1, imin(cdiv(cdiv(L.n, 32), 256), (int64_t)sm_count() * 8));
     note_launch();

@@ -343,6 +343,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// true in every thread of the last CTA of the grid to get here; the fences make all
+// CTAs' earlier global writes (histogram atomics, counts) visible to it
+__device__ __forceinline__ bool last_cta(uint32_t* counter) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
 __device__ __forceinline__ void flag(uint32_t* err, bool bad, uint32_t bit) {
   const unsigned any = __ballot_sync(__activemask(), bad);
   if (any && (threadIdx.x & 31) == __ffs(any) - 1) atomicOr(err, bit);

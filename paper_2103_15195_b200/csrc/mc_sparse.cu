@@ -92,18 +92,6 @@ __device__ __forceinline__ uint64_t block_exscan(uint64_t v, uint64_t* total) {
   return r;
 }
 
-// true in every thread of the last CTA of the grid to get here; the fences make all
-// CTAs' earlier global writes (histogram atomics, counts) visible to it
-__device__ __forceinline__ bool last_cta(uint32_t* counter) {
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (s_last) __threadfence();
-  return s_last;
-}
-
 __device__ __forceinline__ int64_t take_ticket(uint32_t* ticket) {
   __shared__ int64_t s_bid;
   if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
