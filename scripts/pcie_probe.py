@@ -45,9 +45,21 @@ def both():
     d2h()
 
 
+def both_chunked(chunk=1 << 21):
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        with torch.cuda.stream(s1):
+            d_a[a:b].copy_(h_in[a:b], non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out[a:b].copy_(d_b[a:b], non_blocking=True)
+
+
 B = 4 * n
 r = {}
-for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
+for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both), ("both_chunked_8MB", both_chunked),
+                 ("both_chunked_2MB", lambda: both_chunked(1 << 19))):
     ms = timed(fn)
     r[name] = {"ms": ms, "GBps_each_way": B / ms / 1e6}
 r["e2e_bound_fp32_GBps"] = B / r["both"]["ms"] / 1e6
