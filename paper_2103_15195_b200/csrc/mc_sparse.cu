@@ -5,6 +5,12 @@
 // Reference: _compress compressors.py:272-289, randk :278-285, EF :409-413, decode
 // :439-448, aggregate :519-532.  Tie contract for top-k: among
 // equal |x| at the k-th boundary the LOWEST indices are kept.
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
 #include "mc_internal.cuh"
 
 namespace mc {
@@ -864,7 +870,14 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
 //   emit    one CTA per window re-walks from its exact t_w and writes draws[step];
 //   fallback if t_w ever leaves [L_w, L_w + DW) (a > 7 sigma excursion) the single-CTA
 //           walker finishes the stream from that window.
-constexpr int WP = 1024, DW = 512, RX = 32;
+constexpr int WP = 1024;
+// RX: most rejections one 1024-position window may hold (tables entries and the emit
+// re-walk).  A draw for range excl is rejected with p < excl / 2^32, so a window averages
+// up to 1024 n / 2^32 rejections (33 for a 138M-element group): RX = 32 / 64 / 96 by size
+// DW (speculated entering offsets per window) is 512, or 1024 when the walk's drift is
+// large: the offset's deviation from its expectation is a sum of Bernoulli rejections with
+// sd ~ sqrt(k * (n - k/2) / 2^33) (149 for a 138M-element group at 1%), and a window range
+// of +-DW/2 must cover it or the serial walker takes over
 
 struct WalkCtl {
   int64_t fail_base, fail_t0;  // fallback start (fail_base < 0: none)
@@ -903,6 +916,7 @@ __global__ void k_randk_expect(RP p, double* expw, int64_t nwin) {
 }
 
 constexpr int HQ = 16;  // queued filter hits per thread (mean ~3.2 at 1% density)
+template <int DW, int RX>
 __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, const double* expw, int64_t* Lw,
                                uint8_t* tables) {
   extern __shared__ uint32_t masks[];  // [DW + RX][32] then the hit queues [1024][HQ] u16
@@ -983,6 +997,7 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
 // groups (nwin / CG dependent lookups instead of nwin) and replays every group's windows
 // from its exact entering offset in parallel, writing tin[w].
 constexpr int CG = 16;
+template <int DW>
 __global__ void __launch_bounds__(DW) k_randk_compose(const int64_t* Lw, const uint8_t* tables, int64_t nwin,
                                                       int* comp) {
   const int64_t g = blockIdx.x, w0 = g * CG;
@@ -996,6 +1011,7 @@ __global__ void __launch_bounds__(DW) k_randk_compose(const int64_t* Lw, const u
   comp[g * DW + threadIdx.x] = t;
 }
 
+template <int DW>
 __global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, const uint8_t* tables, int64_t nwin,
                                                       const int* comp, int* tg, int64_t* tin, WalkCtl* ctl) {
   __shared__ int s_ng, s_fail_g;
@@ -1047,6 +1063,7 @@ __global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, c
   }
 }
 
+template <int RX>
 __global__ void __launch_bounds__(1024) k_randk_emit_draws(RP p, const uint32_t* words, int64_t nwords,
                                                            const int64_t* tin, const WalkCtl* ctl) {
   __shared__ uint32_t smask[RX][32];
@@ -1458,6 +1475,38 @@ int encode_threshold(const EncodeArgs& a, float* out) {
   return MC_OK;
 }
 
+struct RandkStats {
+  double sd, window_mean_max;
+};
+// Lemire rejection probability of step s is ((2^32 - excl) mod excl) / 2^32 (a sawtooth in
+// excl); summed over the k steps it gives the variance of the walk's drift, and its
+// 1024-step sliding sums the per-window means.  O(k) on the host, cached per group shape.
+RandkStats randk_stats(int64_t n, int64_t k, bool tail_shuffle) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, int64_t, bool>, RandkStats> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(n, k, tail_shuffle);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  std::vector<double> pr((size_t)k);
+  double var = 0.0;
+  for (int64_t st = 0; st < k; ++st) {
+    const uint64_t ex = tail_shuffle ? (uint64_t)(n - st) : (uint64_t)(n - k + 1 + st);
+    const double pv = (double)((0x100000000ull - ex) % ex) / 4294967296.0;
+    pr[(size_t)st] = pv;
+    var += pv * (1.0 - pv);
+  }
+  double win = 0.0, best = 0.0;
+  for (int64_t st = 0; st < k; ++st) {
+    win += pr[(size_t)st];
+    if (st >= WP) win -= pr[(size_t)(st - WP)];
+    best = win > best ? win : best;
+  }
+  const RandkStats r{sqrt(var), best};
+  cache.emplace(key, r);
+  return r;
+}
+
 int encode_randk(const EncodeArgs& a, float* out) {
   const int64_t n = a.n, k = top_k_count(a.spec->sparsity, n);
   RP p{};
@@ -1500,25 +1549,44 @@ int encode_randk(const EncodeArgs& a, float* out) {
     int64_t* tin = reinterpret_cast<int64_t*>(wsb + 2 * a16(8 * nwin));
     WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + 3 * a16(8 * nwin));
     uint8_t* tables = wsb + 3 * a16(8 * nwin) + 64;
-    int* comp = reinterpret_cast<int*>(tables + a16(nwin * DW));           // [ngroups][DW]
-    int* tg = comp + cdiv(nwin, CG) * DW;                                    // [ngroups]
+    // exact drift statistics of this (n, k) stream, once per group shape: sd of the total
+    // rejections and the largest mean rejection count of a 1024-draw window
+    const RandkStats rs = randk_stats(n, k, p.tail_shuffle != 0);
+    const int DWr = rs.sd > 100.0 ? 1024 : 512;  // +-256 covers >= 2.56 sd; the rest falls back
+    const double mu = rs.window_mean_max;
+    auto tail = [&](int r) {  // P(Poisson(mu) >= r) over all windows
+      double term = exp(-mu), sum = 0.0;
+      for (int j = 1; j <= r; ++j) term *= mu / j;
+      for (int j = r; j < r + 400 && term > 1e-300; ++j) { sum += term; term *= mu / (j + 1); }
+      return sum * (double)nwin;
+    };
+    const int RXr = tail(32) < 1e-6 ? 32 : tail(64) < 1e-6 ? 64 : 96;
+    int* comp = reinterpret_cast<int*>(tables + a16(nwin * DWr));           // [ngroups][DW]
+    int* tg = comp + cdiv(nwin, CG) * DWr;                                   // [ngroups]
     note_launch(); k_randk_words<<<(unsigned)imax(1, imin(cdiv(nwords, 8 * 256), (int64_t)sm_count() * 4)), 256, 0, st>>>(p, p.w.list, nwords);
-    if (4 * n >= a16(4 * nwords) + 3 * a16(8 * nwin) + 64 + a16(nwin * DW) + 4 * (cdiv(nwin, CG) * (DW + 1))) {  // room for the parallel walk
-      static bool configured = false;
-      const int tsmem = (DW + RX) * 32 * 4 + 1024 * HQ * 2;
-      if (!configured) {
-        if (cudaFuncSetAttribute(k_randk_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem) != cudaSuccess) {
-          set_error("randk walk smem configuration failed");
-          return MC_ECUDA;
-        }
-        configured = true;
-      }
-      note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
-      note_launch(); k_randk_tables<<<(unsigned)nwin, 1024, tsmem, st>>>(p, p.w.list, nwords, expw, Lw, tables);
+    if (4 * n >= a16(4 * nwords) + 3 * a16(8 * nwin) + 64 + a16(nwin * DWr) + 4 * (cdiv(nwin, CG) * (DWr + 1))) {  // room for the parallel walk
       const int64_t ngrp = cdiv(nwin, CG);
-      note_launch(); k_randk_compose<<<(unsigned)ngrp, DW, 0, st>>>(Lw, tables, nwin, comp);
-      note_launch(); k_randk_chain<<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, tg, tin, ctl);
-      note_launch(); k_randk_emit_draws<<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);
+      note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
+#define MC_RANDK_WALK(DWV, RXV)                                                                                    \
+  {                                                                                                               \
+    const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2;                                                          \
+    static bool cfg = false; /* idempotent attribute set (benign race) */                                          \
+    if (!cfg) {                                                                                                   \
+      MC_API_CHECK(cudaFuncSetAttribute(k_randk_tables<DWV, RXV>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts)); \
+      cfg = true;                                                                                                 \
+    }                                                                                                             \
+    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, expw, Lw, tables); \
+    note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp);                      \
+    note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, tg, tin, ctl);                   \
+    note_launch(); k_randk_emit_draws<RXV><<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);           \
+  }
+      if (DWr == 512 && RXr == 32) MC_RANDK_WALK(512, 32)
+      else if (DWr == 512 && RXr == 64) MC_RANDK_WALK(512, 64)
+      else if (DWr == 512) MC_RANDK_WALK(512, 96)
+      else if (RXr == 32) MC_RANDK_WALK(1024, 32)
+      else if (RXr == 64) MC_RANDK_WALK(1024, 64)
+      else MC_RANDK_WALK(1024, 96)
+#undef MC_RANDK_WALK
       note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, &ctl->fail_base);
     } else {
       note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, nullptr);
