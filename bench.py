@@ -257,10 +257,17 @@ def main():
 
     rank, world, local = dist_env()
     assert world == args.gpus or world == 1, f"WORLD_SIZE={world} but --gpus {args.gpus}"
+    # one process per GPU; MC_BENCH_BACKEND=gloo lets several ranks share one GPU (payloads
+    # staged through host memory) to exercise the multi-rank flow where only one GPU exists
+    backend = os.environ.get("MC_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     spec = spec_for(args)
     prof = gradsets.profile(args.gradset)
     D = prof.total_size

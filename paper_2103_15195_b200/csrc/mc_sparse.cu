@@ -21,13 +21,20 @@ constexpr int ITEMS = 16;       // consecutive elements per thread
 constexpr int TILE = TB * ITEMS;
 
 // ------------------------------------------------------------------ workspace layout
+// top-k radix select over the 31-bit magnitude key: 11 / 11 / 9 bits (a 12-bit first
+// level measured no faster: the candidate list is not what bounds the later passes)
+constexpr int H1B = 11, H2B = 11, H3B = 9;
+constexpr int NB1 = 1 << H1B, NB2 = 1 << H2B, NB3 = 1 << H3B;
+constexpr int S1 = 31 - H1B, S2 = S1 - H2B;
+static_assert(S2 == H3B, "the three levels cover the 31-bit key");
+
 struct SparseWS {
   uint32_t* keys;     // [n]  float bits of the corrected c32
   uint32_t* list;     // [n]  top-k: per-tile candidate segments (tile t's at its first element); randk scratch
   uint32_t* list2;    // [n]  top-k: the segments concatenated in order (the candidate list)
   uint32_t* segcnt;   // [ntiles + 1] top-k: candidates per pass-2 tile, then their exclusive prefix
   uint32_t* cmax;     // [ceil(n/128)] top-k: max |c32| key per 128-element chunk
-  uint32_t* hist;     // [2048 + 2048 + 512]
+  uint32_t* hist;     // [NB1 + NB2 + NB3] radix-select histograms (top-k)
   uint32_t* ctl;      // control words (see CTL_*)
   uint32_t* ticket;   // look-back ticket(s)
   uint64_t* status;   // look-back status [nblk]
@@ -56,7 +63,7 @@ SparseWS carve(uint8_t* w, int64_t n, int64_t k) {
   s.list2 = reinterpret_cast<uint32_t*>(w); w += a16(4 * n);
   s.segcnt = reinterpret_cast<uint32_t*>(w); w += a16(4 * (cdiv(n, 8192) + 1));
   s.cmax = reinterpret_cast<uint32_t*>(w); w += a16(4 * cdiv(n, 128));
-  s.hist = reinterpret_cast<uint32_t*>(w); w += a16(4 * (2048 + 2048 + 512));
+  s.hist = reinterpret_cast<uint32_t*>(w); w += a16(4 * (NB1 + NB2 + NB3));
   s.ctl = reinterpret_cast<uint32_t*>(w); w += a16(4 * CTL_WORDS);
   s.ticket = reinterpret_cast<uint32_t*>(w); w += 16;
   s.status = reinterpret_cast<uint64_t*>(w); w += a16(8 * nblk);
@@ -157,8 +164,8 @@ __device__ __forceinline__ uint32_t key_at(const TP& p, int64_t e) {
 __device__ void select_bin(const uint32_t* hist, int nb, uint32_t k, uint32_t* out_bin, uint32_t* out_krem);
 
 __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
-  __shared__ uint32_t h[2048];
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) h[i] = 0;
+  __shared__ uint32_t h[NB1];
+  for (int i = threadIdx.x; i < NB1; i += blockDim.x) h[i] = 0;
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   bool bad = false;
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
       c[q] = p.pro.r ? __dadd_rn((double)w, rv[q]) : (double)w;
       const float c32 = p.pro.r ? __double2float_rn(c[q]) : w;
       key[q] = __float_as_uint(c32);
-      if (in) atomicAdd(&h[(key[q] & 0x7fffffffu) >> 20], 1u);
+      if (in) atomicAdd(&h[(key[q] & 0x7fffffffu) >> S1], 1u);
     }
     {  // the warp's 128 consecutive elements form one chunk: record their max magnitude key
       uint32_t km = 0;
@@ -233,11 +240,11 @@ __global__ void __launch_bounds__(256) k_topk_pass1(TP p) {
   }
   flag(p.err, bad, MC_ERR_NONFINITE);
   __syncthreads();
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+  for (int i = threadIdx.x; i < NB1; i += blockDim.x)
     if (h[i]) atomicAdd(&p.w.hist[i], h[i]);
   if (last_cta(&p.w.ctl[CTL_DONE1])) {  // select1: the bin holding the k-th largest
     __shared__ uint32_t s_b, s_r;
-    select_bin(p.w.hist, 2048, (uint32_t)p.k, &s_b, &s_r);
+    select_bin(p.w.hist, NB1, (uint32_t)p.k, &s_b, &s_r);
     __syncthreads();
     if (threadIdx.x == 0) { p.w.ctl[CTL_B1] = s_b; p.w.ctl[CTL_KREM1] = s_r; }
   }
@@ -333,10 +340,10 @@ __device__ __forceinline__ uint64_t cta_chunk_prefix(uint64_t warp_total, uint64
 // look-back chain over 12K tiles costs more than the whole read).  Only 128-element chunks
 // whose pass-1 maximum reaches bin B1 are read at all.
 __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
-  __shared__ uint32_t h2[2048];
+  __shared__ uint32_t h2[NB2];
   __shared__ uint32_t s_wt[8];
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) h2[i] = 0;
-  const uint32_t B1 = p.w.ctl[CTL_B1], thr = B1 << 20;
+  for (int i = threadIdx.x; i < NB2; i += blockDim.x) h2[i] = 0;
+  const uint32_t B1 = p.w.ctl[CTL_B1], thr = B1 << S1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bid = blockIdx.x;
   const int64_t nchunks = cdiv(p.n, 128);
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
       const uint32_t key = kk[i][q] & 0x7fffffffu;
       const bool in = c0 + 128 * i + 4 * lane + q < p.n;
       keep |= (uint32_t)(in && key >= thr) << (4 * i + q);
-      if (in && (key >> 20) == B1) atomicAdd(&h2[(key >> 9) & 0x7ffu], 1u);
+      if (in && (key >> S1) == B1) atomicAdd(&h2[(key >> S2) & (NB2 - 1)], 1u);
     }
   }
   const uint32_t wtot = __reduce_add_sync(FULL, __popc(keep));
@@ -402,8 +409,8 @@ __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
     }
   }
   if (threadIdx.x == 0) p.w.segcnt[bid] = tot;
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
-    if (h2[i]) atomicAdd(&p.w.hist[2048 + i], h2[i]);
+  for (int i = threadIdx.x; i < NB2; i += blockDim.x)
+    if (h2[i]) atomicAdd(&p.w.hist[NB1 + i], h2[i]);
 }
 
 // hist3: every CTA turns the pass-2 tile counts into their exclusive prefix in shared
@@ -415,11 +422,11 @@ __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
 constexpr int64_t H3_MAX_TILES = 48 * 1024;  // 192 KB of prefix in smem: groups <= 402M elements
 __global__ void __launch_bounds__(256) k_topk_hist3(TP p, int64_t ntiles) {
   extern __shared__ uint32_t pre[];  // [ntiles + 1]
-  __shared__ uint32_t h3[512];
+  __shared__ uint32_t h3[NB3];
   __shared__ uint32_t s_b2, s_krem;
-  for (int i = threadIdx.x; i < 512; i += blockDim.x) h3[i] = 0;
+  for (int i = threadIdx.x; i < NB3; i += blockDim.x) h3[i] = 0;
   for (int64_t t = threadIdx.x; t < ntiles; t += blockDim.x) pre[t] = p.w.segcnt[t];
-  select_bin(p.w.hist + 2048, 2048, p.w.ctl[CTL_KREM1], &s_b2, &s_krem);  // (ends in a barrier)
+  select_bin(p.w.hist + NB1, NB2, p.w.ctl[CTL_KREM1], &s_b2, &s_krem);  // (ends in a barrier)
   __syncthreads();
   // exclusive scan in place: thread t owns a run of `per` consecutive tiles
   const int64_t per = cdiv(ntiles, 256);
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(256) k_topk_hist3(TP p, int64_t ntiles) {
     p.w.ctl[CTL_B2] = s_b2;
     p.w.ctl[CTL_KREM2] = s_krem;
   }
-  const uint32_t hi = (p.w.ctl[CTL_B1] << 11) | s_b2;
+  const uint32_t hi = (p.w.ctl[CTL_B1] << H2B) | s_b2;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
     int64_t lo = 0, up = ntiles;  // largest t with pre[t] <= j
     while (up - lo > 1) {
@@ -447,17 +454,17 @@ __global__ void __launch_bounds__(256) k_topk_hist3(TP p, int64_t ntiles) {
     const uint32_t e = p.w.list[lo * CB + (j - pre[lo])];
     p.w.list2[j] = e;
     const uint32_t key = key_at(p, e) & 0x7fffffffu;
-    if ((key >> 9) == hi) atomicAdd(&h3[key & 0x1ffu], 1u);
+    if ((key >> S2) == hi) atomicAdd(&h3[key & (NB3 - 1)], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 512; i += blockDim.x)
-    if (h3[i]) atomicAdd(&p.w.hist[4096 + i], h3[i]);
+  for (int i = threadIdx.x; i < NB3; i += blockDim.x)
+    if (h3[i]) atomicAdd(&p.w.hist[NB1 + NB2 + i], h3[i]);
   if (last_cta(&p.w.ctl[CTL_DONE3])) {
     __shared__ uint32_t s_b3, s_need;
-    select_bin(p.w.hist + 4096, 512, p.w.ctl[CTL_KREM2], &s_b3, &s_need);
+    select_bin(p.w.hist + NB1 + NB2, NB3, p.w.ctl[CTL_KREM2], &s_b3, &s_need);
     __syncthreads();
     if (threadIdx.x == 0) {
-      p.w.ctl[CTL_T] = (p.w.ctl[CTL_B1] << 20) | (p.w.ctl[CTL_B2] << 9) | s_b3;
+      p.w.ctl[CTL_T] = (p.w.ctl[CTL_B1] << S1) | (p.w.ctl[CTL_B2] << S2) | s_b3;
       p.w.ctl[CTL_NEED] = s_need;
     }
   }

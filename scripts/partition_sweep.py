@@ -35,6 +35,7 @@ def step_ms(sync, g, steps):
     tot = 0.0
     for _ in range(steps):
         sync.flat.copy_(g)  # the averaged gradient replaces the input in place: restore it
+        torch.cuda.synchronize()  # (the restore is not part of the timed step)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(sync.stream)
         sync.step()
