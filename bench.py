@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--search-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="elements per pipelined H2D/encode/D2H chunk")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: fused encode + push over NVLink peer memory (falls back to NCCL if the "
+                         "peer mapping fails on any rank) or the NCCL allgather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU oracle sample budget")
     ap.add_argument("--json-out", default=None)
@@ -273,6 +276,11 @@ def main():
     D = prof.total_size
 
     sync = GradSync(spec, prof, root_seed=0, device=dev)
+    exchange_used = "none (one rank)"
+    if world > 1:
+        exchange_used = "nccl allgather"
+        if args.exchange == "p2p" and sync.try_peer_exchange():
+            exchange_used = "encode fused with push over peer memory (CUDA IPC, NVLink)"
     host_grads = torch.from_numpy(gradsets.synthetic_gradients(args.gradset, 0, rank)).pin_memory()
     sync.flat.copy_(host_grads)
     torch.cuda.synchronize()
@@ -398,7 +406,8 @@ def main():
                 "group_sizes": sizes,
                 "search": None if search is None else {"evaluations": search.evaluations,
                                                        "termination": search.termination, "F_ms": search.F_ms},
-                "parallelism": f"dp{world} (allgather of compressed payloads over NCCL)",
+                "parallelism": f"dp{world}",
+                "exchange": exchange_used,
                 "l2": "inputs larger than L2 (grads 4D + fp64 residual 8D bytes per rank, >> 126 MB)",
                 "input": "step t+1 encodes the averaged gradient written by step t (in place)",
             },

@@ -44,6 +44,7 @@ extern "C" {
 #define MC_ERR_INDEX_RANGE 0x2u  /* "corrupt payload: index out of range"   compressors.py:444 */
 #define MC_ERR_INDEX_ORDER 0x4u  /* "corrupt payload: indices not increasing" compressors.py:445 */
 #define MC_ERR_HEADER 0x8u       /* payload header does not match spec / length */
+#define MC_ERR_PEER_TIMEOUT 0x10u /* mc_push_wait: a peer's payload did not arrive (~10 s) */
 
 /* algorithm ids == position in the reference ALGORITHMS tuple (compressors.py:29-43) */
 enum {
@@ -142,6 +143,21 @@ int mc_unpack(const float* fused, float* const* dsts, const int64_t* numels, int
  * the stream for data-dependent (threshold) payloads. */
 int mc_serialize(const mc_spec* spec, const void* payload, int64_t n, void* out, int64_t out_cap,
                  int64_t* out_len, void* stream);
+
+/* Encode fused with the allgather over peer memory (NVLink P2P / symmetric memory): the
+ * payload is written to `payload` (this rank's slot of its own gather buffer) and to every
+ * dsts[j] (this rank's slot in rank j's gather buffer; host array of nranks device / peer-
+ * mapped pointers, the entry equal to `payload` is the local one); when all of it is
+ * system-visible, *flags[j] := epoch for every j (rank j's flag word for this rank).  The
+ * pipe-kernel codecs (efsignsgd, onebit, int8) store into the peer slots from the encode
+ * kernel itself; the others encode, then copy.  mc_push_wait: the stream waits until the
+ * local flags[0..nranks) all equal epoch — the gathered payloads are then complete in rank
+ * order, exactly what mc_decode_mean reads (replaces the NCCL allgather of trainer.py:377-389). */
+int mc_encode_push(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+                   uint64_t key_lo, uint64_t key_hi, void* payload, void* const* dsts, uint32_t* const* flags,
+                   int32_t nranks, uint32_t epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                   void* stream);
+int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint32_t* err_flags, void* stream);
 
 /* Host-buffer sync of one rank (world size 1), enqueued natively: the trainer's step on a
  * worker's host gradient (trainer.py:360-395, one worker).  For each group: H2D of

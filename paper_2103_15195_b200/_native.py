@@ -21,6 +21,7 @@ MC_ERR_NONFINITE = 0x1
 MC_ERR_INDEX_RANGE = 0x2
 MC_ERR_INDEX_ORDER = 0x4
 MC_ERR_HEADER = 0x8
+MC_ERR_PEER_TIMEOUT = 0x10
 
 
 class McLayout(ctypes.Structure):
@@ -63,6 +64,10 @@ _SIGS = {
     "mc_pack": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P, _P]),
     "mc_unpack": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P]),
     "mc_serialize": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), _P]),
+    "mc_encode_push": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, ctypes.c_uint64, ctypes.c_uint64, _P,
+                                      ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_uint32, _P,
+                                      ctypes.c_int64, _P, _P]),
+    "mc_push_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P]),
     "mc_pipe_create": (ctypes.c_int, [ctypes.POINTER(_P)]),
     "mc_pipe_destroy": (None, [_P]),
     "mc_pipe_group": (ctypes.c_int, [_P, _SPEC, _P, _P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, ctypes.c_uint64,

@@ -254,6 +254,40 @@ def device_encode_decode(spec: CompressorSpec, grad: torch.Tensor, residual: Opt
     return DevicePayload(spec, n, payload, L)
 
 
+def device_encode_push(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],
+                       momentum: Optional[torch.Tensor], seed: int, payload: torch.Tensor, dsts: Sequence[int],
+                       flags: Sequence[int], epoch: int, err: Optional[torch.Tensor] = None, stream=None,
+                       cspec=None) -> None:
+    """Encode into ``payload`` (this rank's slot of its own gather buffer) and push the same
+    bytes into every peer slot ``dsts[j]`` (device / peer-mapped addresses, one per rank, the
+    own slot included), then release ``flags[j]`` := epoch — the allgather over peer memory
+    fused with the encode (mc_encode_push).  Pair with ``push_wait`` before decoding."""
+    n = grad.numel()
+    cs = cspec if cspec is not None else spec.to_c()
+    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n))
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=grad.device)
+    lo, hi = split_seed(seed)
+    k = len(dsts)
+    arr_d = (ctypes.c_void_p * k)(*dsts)
+    arr_f = (ctypes.c_void_p * k)(*flags)
+    _native.check(
+        _native.lib().mc_encode_push(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum), lo, hi,
+                                     payload.data_ptr(), arr_d, arr_f, k, int(epoch) & 0xFFFFFFFF, ws.data_ptr(),
+                                     ws.numel(), err.data_ptr(), _stream_ptr(stream)),
+        "mc_encode_push",
+    )
+
+
+def push_wait(flags: torch.Tensor, nranks: int, epoch: int, err: Optional[torch.Tensor] = None, stream=None) -> None:
+    """The stream waits until all ``nranks`` local flag words equal ``epoch`` (mc_push_wait);
+    a peer silent for ~10 s sets MC_ERR_PEER_TIMEOUT in ``err`` instead of hanging."""
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=flags.device)
+    _native.check(_native.lib().mc_push_wait(flags.data_ptr(), nranks, int(epoch) & 0xFFFFFFFF, err.data_ptr(),
+                                             _stream_ptr(stream)), "mc_push_wait")
+
+
 def device_decode_mean(spec: CompressorSpec, base: torch.Tensor, stride: int, nranks: int, n: int,
                        out: torch.Tensor, err: torch.Tensor, stream=None, cspec=None) -> None:
     cs = cspec if cspec is not None else spec.to_c()
@@ -271,6 +305,8 @@ def _raise_flags(flags: int) -> None:
         raise ValueError("corrupt payload: index out of range")
     if flags & _native.MC_ERR_INDEX_ORDER:
         raise ValueError("corrupt payload: indices not increasing")
+    if flags & _native.MC_ERR_PEER_TIMEOUT:
+        raise RuntimeError("peer exchange: a rank's payload did not arrive (mc_push_wait timed out)")
     if flags & _native.MC_ERR_HEADER:
         raise ValueError("corrupt payload: header does not match spec")
 

@@ -191,7 +191,9 @@ int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t 
 
 static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
                        uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
-                       uint32_t* err_flags, void* stream, float* out, int64_t begin = 0, int64_t count = -1) {
+                       uint32_t* err_flags, void* stream, float* out, int64_t begin = 0, int64_t count = -1,
+                       int npush = 0, void* const* push_dsts = nullptr, uint32_t* const* push_flags = nullptr,
+                       uint32_t epoch = 0) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
   if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
@@ -219,6 +221,10 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
   a.ctx.err = err_flags;
   a.begin = begin;
   a.count = count;
+  a.npush = npush;
+  a.push_dsts = push_dsts;
+  a.push_flags = push_flags;
+  a.epoch = epoch;
   if (begin != 0 || (count >= 0 && count != n)) {  // chunked: deterministic elementwise / bucketed codecs only
     const int al = s->algorithm;
     if (begin < 0 || count < 1 || begin + count > n) { set_error("bad chunk [%lld, +%lld)", (long long)begin, (long long)count); return MC_EINVAL; }
@@ -227,10 +233,13 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
       return MC_EINVAL;
     }
   }
+  if (npush && !(s->algorithm == MC_EFSIGNSGD || s->algorithm == MC_ONEBIT || s->algorithm == MC_INT8))
+    return MC_FUSED_UNSUPPORTED;  // only the pipe kernel stores into peer slots itself
   switch (s->algorithm) {
     case MC_IDENTITY: case MC_FP16: return encode_elementwise(a, out);
     case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: {
       const int rc = encode_bucketed(a, out);
+      if (npush) return rc;  // MC_FUSED_UNSUPPORTED: nothing launched, the caller encodes + copies
       return (rc == MC_FUSED_UNSUPPORTED && !out) ? MC_OK : rc;
     }
     case MC_SIGNSGD: case MC_SIGNUM: { const int rc = encode_sign_global(a); return rc == MC_OK && out ? MC_FUSED_UNSUPPORTED : rc; }
@@ -249,6 +258,105 @@ int mc_encode(const mc_spec* s, const float* grad, int64_t n, double* residual, 
               void* stream) {
   return encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes, err_flags,
                      stream, nullptr);
+}
+
+}  // extern "C"
+
+namespace mc {
+namespace {
+struct PushArgs {
+  const uint8_t* src;
+  int64_t bytes;  // multiple of 16 (payload layouts are 16-byte sections)
+  int ndst, nflag;
+  uint8_t* dst[MC_MAX_PUSH];
+  uint32_t* flag[MC_MAX_PUSH];
+  uint32_t epoch;
+  uint32_t* done;
+};
+// Copy a finished payload into every peer slot (16-byte vectors, all CTAs), then the last
+// CTA releases every rank's flag for this rank at system scope.
+__global__ void __launch_bounds__(256) k_push_copy(PushArgs a) {
+  const int64_t nv = a.bytes / 16;
+  const uint4* src = reinterpret_cast<const uint4*>(a.src);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = src[i];
+    for (int j = 0; j < a.ndst; ++j) reinterpret_cast<uint4*>(a.dst[j])[i] = v;
+  }
+  __threadfence_system();
+  if (last_cta(a.done)) {
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int j = 0; j < a.nflag; ++j) st_release_sys(a.flag[j], a.epoch);
+    }
+  }
+}
+// Wait (one CTA) until every flag equals the epoch: the gathered payloads are complete.
+// Bounded (~10 s): a peer that never signals raises MC_ERR_PEER_TIMEOUT instead of hanging.
+__global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch, uint32_t* err) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(flags + i) != epoch) {
+      __nanosleep(256);
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) { atomicOr(err, MC_ERR_PEER_TIMEOUT); break; }
+    }
+  }
+  __syncthreads();
+}
+}  // namespace
+
+int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a, cudaStream_t st) {
+  PushArgs pa{};
+  pa.src = payload;
+  pa.bytes = (bytes + 15) / 16 * 16;
+  for (int j = 0; j < a.npush; ++j) {
+    pa.flag[pa.nflag++] = a.push_flags[j];
+    if (a.push_dsts[j] != (void*)payload) pa.dst[pa.ndst++] = static_cast<uint8_t*>(a.push_dsts[j]);
+  }
+  pa.epoch = a.epoch;
+  pa.done = reinterpret_cast<uint32_t*>(a.ws);  // the encode is complete in stream order: its scratch is free
+  MC_API_CHECK(cudaMemsetAsync(pa.done, 0, 4, st));
+  const unsigned g = (unsigned)imax(1, imin(cdiv(pa.bytes / 16, 256), (int64_t)sm_count() * 4));
+  note_launch();
+  k_push_copy<<<g, 256, 0, st>>>(pa);
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+}  // namespace mc
+
+extern "C" {
+
+int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                   uint64_t key_lo, uint64_t key_hi, void* payload, void* const* dsts, uint32_t* const* flags,
+                   int32_t nranks, uint32_t epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                   void* stream) {
+  if (nranks < 1 || nranks > MC_MAX_PUSH || !dsts || !flags) { set_error("bad push destinations"); return MC_EINVAL; }
+  const int rc = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
+                             err_flags, stream, nullptr, 0, -1, nranks, dsts, flags, epoch);
+  if (rc != MC_FUSED_UNSUPPORTED) return rc;
+  // this codec's kernels do not push: plain encode, then the peer copy + flags
+  const int rc2 = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
+                              err_flags, stream, nullptr);
+  if (rc2 != MC_OK) return rc2;
+  mc_layout L;
+  if (fill_layout(s, n, 0, &L) != MC_OK) return MC_EINVAL;
+  EncodeArgs a{};
+  a.ws = static_cast<uint8_t*>(workspace);
+  a.npush = nranks;
+  a.push_dsts = dsts;
+  a.push_flags = flags;
+  a.epoch = epoch;
+  return launch_push_copy(static_cast<const uint8_t*>(payload), L.bytes, a, static_cast<cudaStream_t>(stream));
+}
+
+int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint32_t* err_flags, void* stream) {
+  if (!flags || nranks < 1 || !err_flags) { set_error("bad flags"); return MC_EINVAL; }
+  note_launch();
+  k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, epoch, err_flags);
+  MC_LAUNCH_CHECK();
+  return MC_OK;
 }
 
 int mc_encode_range(const mc_spec* s, const float* grad, int64_t n, int64_t begin, int64_t count, double* residual,

@@ -400,7 +400,27 @@ struct EncodeArgs {
   Ctx ctx;
   int64_t begin = 0;   // chunked encode: process elements [begin, begin + count) of the group
   int64_t count = -1;  // -1: the whole group
+  // peer push (fused allgather over NVLink peer memory, mc_encode_push): the payload bytes
+  // are also stored at push_dsts[j] (this rank's slot in rank j's gather buffer, a peer-
+  // mapped device pointer; the entry equal to `payload` is skipped) and, once every CTA's
+  // stores are system-visible, push_flags[j] (rank j's flag word for this rank) := epoch
+  int npush = 0;
+  void* const* push_dsts = nullptr;       // host array [npush] of device pointers
+  uint32_t* const* push_flags = nullptr;  // host array [npush] of device pointers
+  uint32_t epoch = 0;
 };
+
+constexpr int MC_MAX_PUSH = 16;
+// release-store of one flag word at system scope (readers poll with ld.acquire.sys)
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a, cudaStream_t st);
 
 int64_t bucket_ws_bytes(const mc_spec* s, int64_t n);
 int64_t sparse_ws_bytes(const mc_spec* s, int64_t n);

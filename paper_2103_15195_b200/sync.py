@@ -196,6 +196,127 @@ class GradSync:
     def drop_graph(self) -> None:
         self._graph = None
 
+    # ------------------------------------------------------------ allgather over peer memory
+    def use_peer_exchange(self, backend: str = "ipc") -> None:
+        """Replace the NCCL allgather by the fused encode + push over peer memory
+        (mc_encode_push / mc_push_wait): each group has two gather buffers (alternating by
+        exchange epoch) and flag words that every rank maps — ``backend="ipc"`` shares them
+        with CUDA IPC handles (torch.multiprocessing's reductions, exchanged over the process
+        group; peer-mapped over NVLink, and also valid for several processes on one GPU),
+        ``"symm"`` uses torch symmetric memory.  Each rank's encode kernel stores its payload
+        straight into its slot of every rank's buffer and releases their flags when done.
+        Double buffering is enough: a rank pushes epoch e+2 into the buffer a peer read at
+        epoch e only after that peer's epoch-(e+1) push, which its stream issued after its
+        decode of epoch e.  Fixed-size payloads (not threshold)."""
+        if self.world < 2:
+            raise ValueError("the peer exchange needs more than one rank")
+        if self.spec.algorithm == "threshold":
+            raise ValueError("threshold payloads are variable-size: use the NCCL exchange")
+        if backend not in ("ipc", "symm"):
+            raise ValueError(f"unknown peer backend {backend!r}")
+        self._peer = {"backend": backend, "groups": {}, "epoch": 0}
+
+    def try_peer_exchange(self, backend: str = "ipc") -> bool:
+        """Collective probe (every rank must call it): map a small buffer of every rank; if
+        that works everywhere, switch this GradSync to the peer exchange and return True,
+        else keep the NCCL allgather.  The collectives run on all ranks whatever fails
+        locally, so a failed probe cannot deadlock."""
+        if self.world < 2 or self.spec.algorithm == "threshold":
+            return False
+        ok = 1
+        self._peer = {"backend": backend, "groups": {}, "epoch": 0}
+        probe = torch.zeros(16, dtype=torch.int32, device=self.device)
+        try:
+            if backend == "symm":
+                raise RuntimeError("probe covers the IPC backend only")
+            from torch.multiprocessing.reductions import reduce_tensor
+
+            handles = [None] * self.world
+            torch.distributed.all_gather_object(handles, reduce_tensor(probe), group=self.pg)
+            for j, (fn, args) in enumerate(handles):
+                if j != self.rank:
+                    self._peer.setdefault("mapped", []).append(fn(*args))
+        except Exception:  # noqa: BLE001 - fall back to NCCL on every rank
+            ok = 0
+        t = torch.tensor([ok], dtype=torch.int32, device=self.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN, group=self.pg)
+        if int(t.item()) == 1:
+            return True
+        self._peer = None
+        return False
+
+    def _share(self, t: torch.Tensor) -> list[int]:
+        """Device addresses of every rank's copy of ``t`` as mapped in this process."""
+        if self._peer["backend"] == "symm":
+            import torch.distributed._symmetric_memory as symm
+
+            h = symm.rendezvous(t, self.pg if self.pg is not None else torch.distributed.group.WORLD)
+            return [int(h.buffer_ptrs[j]) for j in range(self.world)]
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        handles = [None] * self.world
+        torch.distributed.all_gather_object(handles, reduce_tensor(t), group=self.pg)
+        ptrs = []
+        keep = self._peer.setdefault("mapped", [])
+        for j, (fn, args) in enumerate(handles):
+            if j == self.rank:
+                ptrs.append(t.data_ptr())
+            else:
+                peer = fn(*args)  # opens the IPC handle: a tensor over rank j's memory
+                keep.append(peer)
+                ptrs.append(peer.data_ptr())
+        return ptrs
+
+    def _alloc_shared(self, numel: int, dtype) -> torch.Tensor:
+        if self._peer["backend"] == "symm":
+            import torch.distributed._symmetric_memory as symm
+
+            return symm.empty(numel, dtype=dtype, device=self.device)
+        return torch.empty(numel, dtype=dtype, device=self.device)
+
+    def _peer_group(self, key, g: int, grp: _Group):
+        st = self._peer["groups"].get((key, g))
+        if st is None:
+            stride = (grp.layout.bytes + 15) // 16 * 16
+            bufs, dsts = [], []
+            for _ in range(2):
+                b = self._alloc_shared(self.world * stride, torch.uint8)
+                b.zero_()
+                ptrs = self._share(b)
+                bufs.append(b)
+                dsts.append([ptrs[j] + self.rank * stride for j in range(self.world)])
+            fl = self._alloc_shared(2 * self.world, torch.int32)
+            fl.zero_()
+            torch.cuda.synchronize(self.device)
+            fptrs = self._share(fl)
+            flags = [[fptrs[j] + 4 * (par * self.world + self.rank) for j in range(self.world)] for par in range(2)]
+            torch.distributed.barrier(group=self.pg)
+            st = {"stride": stride, "bufs": bufs, "dsts": dsts, "fl": fl, "flags": flags}
+            self._peer["groups"][(key, g)] = st
+        return st
+
+    def _step_peer(self, plan, key) -> None:
+        from .compressors import device_encode_push, push_wait
+
+        self._peer["epoch"] += 1
+        ep = self._peer["epoch"]
+        par = ep & 1
+        pend = []
+        for g, grp in enumerate(plan):  # every encode pushes as it finishes: no collective launch
+            st = self._peer_group(key, g, grp)
+            lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
+            buf = st["bufs"][par]
+            own = buf[self.rank * st["stride"]:(self.rank + 1) * st["stride"]]
+            device_encode_push(self.spec, self.flat[grp.start:grp.end], grp.residual, grp.momentum, lo | (hi << 64),
+                               own, st["dsts"][par], st["flags"][par], ep, err=self.err, stream=self.stream,
+                               cspec=self.cspec)
+            pend.append((grp, st, buf))
+        for grp, st, buf in pend:
+            push_wait(st["fl"][par * self.world:(par + 1) * self.world], self.world, ep, err=self.err,
+                      stream=self.stream)
+            device_decode_mean(self.spec, buf, st["stride"], self.world, grp.n, self.flat[grp.start:grp.end],
+                               self.err, stream=self.stream, cspec=self.cspec)
+
     def step(self, partition: Optional[Partition] = None) -> None:
         """One synchronisation of every group of ``partition`` (default: the pinned one),
         enqueued on the side stream after the gradients' producer stream.
@@ -216,7 +337,9 @@ class GradSync:
         plan = self._plan(part)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
-            if self.world > 1 and self.spec.algorithm != "threshold" and len(plan) > 1:
+            if getattr(self, "_peer", None) is not None:
+                self._step_peer(plan, part.boundaries)
+            elif self.world > 1 and self.spec.algorithm != "threshold" and len(plan) > 1:
                 pending = []
                 for g, grp in enumerate(plan):
                     x = self._encode_group(g, grp)

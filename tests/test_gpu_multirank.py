@@ -25,7 +25,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, kw, q):
+def _rank(rank, world, port, kw, q, peer=False):
     import sys
     from pathlib import Path
 
@@ -43,6 +43,13 @@ def _rank(rank, world, port, kw, q):
         torch.cuda.set_device(0)
         prof = gradsets.profile("tiny40")
         sync = GradSync(CompressorSpec(**kw), prof, partition=Partition(prof.n_tensors, (7, 30)), root_seed=3)
+        if peer:
+            try:
+                sync.use_peer_exchange()
+                sync._peer_group(sync.partition.boundaries, 0, sync._plan(sync.partition)[0])
+            except Exception as exc:  # noqa: BLE001 - symmetric memory unavailable in this setup
+                q.put((rank, "SKIP " + repr(exc)))
+                return
         outs = []
         for it in range(3):
             sync.flat.copy_(torch.from_numpy(gradsets.synthetic_gradients("tiny40", it, rank)))
@@ -57,8 +64,11 @@ def _rank(rank, world, port, kw, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("peer", [False, True], ids=["nccl-path", "peer-push"])
 @pytest.mark.parametrize("kw", SPECS, ids=lambda k: k["algorithm"])
-def test_two_ranks_match_oracle(kw):
+def test_two_ranks_match_oracle(kw, peer):
+    """peer-push: the allgather replaced by mc_encode_push into torch symmetric-memory
+    buffers of both ranks (skipped where symmetric memory cannot be set up)."""
     import torch.multiprocessing as mp
 
     import mergecomp_oracle as O
@@ -69,13 +79,17 @@ def test_two_ranks_match_oracle(kw):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, kw, q)) for r in range(2)]
+    if peer and kw["algorithm"] == "threshold":
+        pytest.skip("threshold payloads are variable-size (NCCL exchange only)")
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, kw, q, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=60)
     for r in (0, 1):
+        if isinstance(res[r], str) and res[r].startswith("SKIP"):
+            pytest.skip(res[r])
         assert not isinstance(res[r], str), res[r]
 
     spec = CompressorSpec(**kw)

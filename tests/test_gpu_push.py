@@ -1,0 +1,57 @@
+"""Allgather over peer memory fused with the encode (mc_encode_push / mc_push_wait), checked
+on one GPU by simulating N ranks: N gather buffers and N flag arrays live on the device; rank
+r encodes its gradient and pushes its payload into slot r of every gather buffer.  Every
+gather buffer must equal, byte for byte, the rank-ordered concatenation an NCCL allgather
+of independently encoded payloads produces, and decode to the same mean."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8", "dgc_lite", "qsgd", "signsgd", "fp16"])
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_encode_push_equals_allgather(algo, nranks):
+    from paper_2103_15195_b200 import _native
+    from paper_2103_15195_b200 import compressors as C
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    spec = CompressorSpec(algo, sparsity=0.999)
+    n = 1_000_003 if algo not in ("efsignsgd", "onebit", "int8") else 1_048_576 + 512 * 7 + 13
+    L = _native.layout(spec.to_c(), n)
+    stride = (L.bytes + 15) // 16 * 16
+    gens = [torch.Generator(device="cuda").manual_seed(100 + r) for r in range(nranks)]
+    grads = [torch.randn(n, device="cuda", generator=g) * 1e-3 for g in gens]
+    ef = spec.uses_error_feedback
+    res_a = [torch.zeros(n, dtype=torch.float64, device="cuda") if ef else None for _ in range(nranks)]
+    res_b = [torch.zeros(n, dtype=torch.float64, device="cuda") if ef else None for _ in range(nranks)]
+    gather = [torch.zeros(nranks * stride, dtype=torch.uint8, device="cuda") for _ in range(nranks)]
+    flags = [torch.zeros(nranks, dtype=torch.int32, device="cuda") for _ in range(nranks)]
+    for epoch in (1, 2):  # two exchanges: state carried, flags re-armed by the epoch
+        for r in range(nranks):
+            own = gather[r][r * stride:(r + 1) * stride]
+            dsts = [gather[j].data_ptr() + r * stride for j in range(nranks)]
+            fl = [flags[j].data_ptr() + 4 * r for j in range(nranks)]
+            C.device_encode_push(spec, grads[r] * epoch, res_a[r], None, 1000 * epoch + r, own, dsts, fl, epoch)
+        for j in range(nranks):
+            C.push_wait(flags[j], nranks, epoch)
+        ref = torch.zeros(nranks * stride, dtype=torch.uint8, device="cuda")
+        for r in range(nranks):
+            C.device_encode(spec, grads[r] * epoch, res_b[r], None, 1000 * epoch + r, out=ref[r * stride:r * stride + L.bytes])
+        torch.cuda.synchronize()
+        for j in range(nranks):
+            assert torch.equal(gather[j], ref), (algo, nranks, epoch, j)
+        if ef:
+            for r in range(nranks):
+                assert torch.equal(res_a[r].view(torch.int64), res_b[r].view(torch.int64))
+        outs = []
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for j in range(nranks):
+            o = torch.empty(n, device="cuda")
+            C.device_decode_mean(spec, gather[j], stride, nranks, n, o, err)
+            outs.append(o)
+        torch.cuda.synchronize()
+        assert int(err.item()) == 0
+        for o in outs[1:]:
+            assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32))
