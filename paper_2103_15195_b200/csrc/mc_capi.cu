@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) k_push_copy(PushArgs a) {
     const uint4 v = src[i];
     for (int j = 0; j < a.ndst; ++j) reinterpret_cast<uint4*>(a.dst[j])[i] = v;
   }
-  __threadfence_system();
+  __threadfence_system();  // this thread's peer stores, system-wide, before the CTA counts in
   if (last_cta(a.done)) {
     if (threadIdx.x == 0) {
       __threadfence_system();

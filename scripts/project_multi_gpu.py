@@ -3,7 +3,9 @@ owns: encode (unfused, payload only) + decode_mean over N gathered payloads (the
 payloads of N different gradient sets stacked exactly like the NCCL allgather
 output).  The allgather itself is estimated from the payload size and the measured
 peer bandwidth (770 GB/s per direction, B200_PROFILING.md); (N-1) * P bytes arrive
-per rank.  Prints one JSON line per (codec, N)."""
+per rank.  The peer-memory path (mc_encode_push: the encode kernel stores into all N
+gather slots) is measured with the N slots on this GPU and projected as
+max(encode_push, allgather) + decode.  Prints one JSON line per (codec, N)."""
 import argparse
 import json
 import sys
@@ -17,8 +19,12 @@ from paper_2103_15195_b200.spec import CompressorSpec  # noqa: E402
 
 
 def timed(fn, reps=20):
+    """Device time per call: a ~5 ms spin kernel keeps the GPU busy while the host enqueues
+    all reps, so host launch overhead never shows up as GPU idle time between the events."""
     for _ in range(3):
         fn()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(10_000_000)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(reps):
@@ -50,9 +56,26 @@ def main():
             t_dec = timed(lambda: C.device_decode_mean(spec, gathered, stride, N, D, out, err))
             t_ag = (N - 1) * P / 770e9 * 1e3
             step = t_enc + t_ag + t_dec
+            # fused encode + push (mc_encode_push) into N gather buffers of this GPU: the kernel
+            # cost of storing into every slot; over NVLink the (N-1)*P bytes need t_ag, which
+            # the push overlaps with the encode, so the p2p step is max(encode_push, t_ag) + decode
+            pstride = (stride + 15) // 16 * 16
+            bufs = [torch.zeros(N * pstride, dtype=torch.uint8, device="cuda") for _ in range(N)]
+            flg = [torch.zeros(N, dtype=torch.int32, device="cuda") for _ in range(N)]
+            ep = [0]
+
+            def push():
+                ep[0] += 1
+                C.device_encode_push(spec, x, res, None, 1, bufs[0][:pstride], [b.data_ptr() for b in bufs],
+                                     [f.data_ptr() for f in flg], ep[0])
+
+            t_push = timed(push)
+            step_p2p = max(t_push, t_ag) + t_dec
             print(json.dumps({"codec": name, "N": N, "encode_ms": round(t_enc, 4), "decode_mean_ms": round(t_dec, 4),
                               "allgather_est_ms": round(t_ag, 4), "step_ms": round(step, 4),
-                              "per_gpu_GBps": round(4 * D / step / 1e6, 1)}), flush=True)
+                              "per_gpu_GBps": round(4 * D / step / 1e6, 1), "encode_push_ms": round(t_push, 4),
+                              "p2p_step_ms": round(step_p2p, 4),
+                              "p2p_per_gpu_GBps": round(4 * D / step_p2p / 1e6, 1)}), flush=True)
 
 
 if __name__ == "__main__":
