@@ -43,9 +43,12 @@ def parse():
     ap.add_argument("--search-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="elements per pipelined H2D/encode/D2H chunk")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
                     help="N > 1: fused encode + push over NVLink peer memory (falls back to NCCL if the "
-                         "peer mapping fails on any rank) or the NCCL allgather")
+                         "peer mapping fails on any rank), the NCCL allgather, or auto: the push where the "
+                         "payload is >= 1/8 of the fp32 gradient (byte codecs, where overlapping the exchange "
+                         "with the encode pays; profiles/r1_projection_multi_gpu.jsonl), NCCL for the 1-bit "
+                         "and sparse codecs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU oracle sample budget")
     ap.add_argument("--json-out", default=None)
@@ -279,7 +282,10 @@ def main():
     exchange_used = "none (one rank)"
     if world > 1:
         exchange_used = "nccl allgather"
-        if args.exchange == "p2p" and sync.try_peer_exchange():
+        from paper_2103_15195_b200.spec import payload_bytes
+
+        want_p2p = args.exchange == "p2p" or (args.exchange == "auto" and payload_bytes(spec, D) * 8 >= 4 * D)
+        if want_p2p and sync.try_peer_exchange():
             exchange_used = "encode fused with push over peer memory (CUDA IPC, NVLink)"
     host_grads = torch.from_numpy(gradsets.synthetic_gradients(args.gradset, 0, rank)).pin_memory()
     sync.flat.copy_(host_grads)
