@@ -903,57 +903,74 @@ __device__ __forceinline__ bool rejects(const RP& p, uint32_t w32, int64_t s) {
   return left < ex && left < (0u - ex) % ex;
 }
 
+// per window: expected rejections (expw[w]) and their variance (expw[nwin + w])
 __global__ void k_randk_expect(RP p, double* expw, int64_t nwin) {
-  __shared__ double part[8];
+  __shared__ double part[8], vpart[8];
   const int64_t w = blockIdx.x;
-  double acc = 0.0;
+  double acc = 0.0, var = 0.0;
   for (int i = threadIdx.x; i < WP; i += blockDim.x) {
     const int64_t s = imin(imax(w * WP + i, 0), p.k - 1);
     const uint32_t ex = excl_of(p, s);
-    acc += (double)((0u - ex) % ex) * 0x1.0p-32;
+    const double pr = (double)((0u - ex) % ex) * 0x1.0p-32;
+    acc += pr;
+    var += pr * (1.0 - pr);
   }
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  for (int o = 16; o; o >>= 1) {
+    acc += __shfl_xor_sync(FULL, acc, o);
+    var += __shfl_xor_sync(FULL, var, o);
+  }
+  if ((threadIdx.x & 31) == 0) { part[threadIdx.x >> 5] = acc; vpart[threadIdx.x >> 5] = var; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    double t = 0.0, v = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { t += part[i]; v += vpart[i]; }
     expw[w] = t;
+    expw[nwin + w] = v;
   }
 }
 
 constexpr int HQ = 16;  // queued filter hits per thread (mean ~3.2 at 1% density)
 template <int DW, int RX>
-__global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, const double* expw, int64_t* Lw,
-                               uint8_t* tables) {
+__global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, const double* expw, int64_t nwin,
+                               int64_t* Lw, uint8_t* tables) {
   extern __shared__ uint32_t masks[];  // [DW + RX][32] then the hit queues [1024][HQ] u16
   uint16_t* hitq = reinterpret_cast<uint16_t*>(masks + (DW + RX) * 32);
   __shared__ int64_t s_L;
-  __shared__ double s_part[32];
+  __shared__ int s_dw;
+  __shared__ double s_part[32], s_vpart[32];
   const int64_t w = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {  // expected offset at the window start: sum of the earlier windows' expectations
-     // (block reduction; the value only centres the speculated range — the chain checks it)
-    double e = 0.0;
-    for (int64_t i = tid; i < w; i += blockDim.x) e += expw[i];
+  {  // expected offset at the window start and its variance: sums over the earlier windows
+     // (block reduction; they only centre and size the speculated range — the chain checks it).
+     // The range is +-(7 sd + 16), at most DW: early windows, whose offset is still nearly
+     // deterministic, evaluate a few dozen entering offsets instead of DW
+    double e = 0.0, v = 0.0;
+    for (int64_t i = tid; i < w; i += blockDim.x) { e += expw[i]; v += expw[nwin + i]; }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
-    if (lane == 0) s_part[warp] = e;
+    for (int o = 16; o; o >>= 1) {
+      e += __shfl_xor_sync(FULL, e, o);
+      v += __shfl_xor_sync(FULL, v, o);
+    }
+    if (lane == 0) { s_part[warp] = e; s_vpart[warp] = v; }
     __syncthreads();
     if (tid == 0) {
-      double t = 0.0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s_part[i];
-      const int64_t L = imax(0, (int64_t)floor(t) - DW / 2);
+      double t = 0.0, vv = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { t += s_part[i]; vv += s_vpart[i]; }
+      const int half = (int)ceil(7.0 * sqrt(vv)) + 16;
+      const int dw = (int)imin(DW, (int64_t)((2 * half + 31) / 32 * 32));
+      const int64_t L = imax(0, (int64_t)floor(t) - dw / 2);
       s_L = L;
+      s_dw = dw;
       Lw[w] = L;
     }
   }
   __syncthreads();
   const int64_t L = s_L;
+  const int dwin = s_dw;
   const Philox ph{p.k0, p.k1};
   const int64_t pos = w * WP + tid;
   const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
-  for (int i = tid; i < (DW + RX) * 32; i += blockDim.x) masks[i] = 0u;
+  for (int i = tid; i < (dwin + RX) * 32; i += blockDim.x) masks[i] = 0u;
   __syncthreads();
   // candidate c serves step s = pos - L - c: lo32(w * excl) moves by -+w and excl by -+1 per
   // candidate, so the "may reject" filter (left < excl, p ~ excl / 2^32 < 1%) is two adds and a
@@ -970,7 +987,7 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
   uint16_t* q = hitq + tid * HQ;
   int nh = 0;
 #pragma unroll 8
-  for (int c = 0; c < DW + RX; ++c) {
+  for (int c = 0; c < dwin + RX; ++c) {
     if (left < ex) {
       if (nh < HQ) q[nh++] = (uint16_t)c;
       else if (rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);  // (never in practice)
@@ -984,7 +1001,7 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
     if (i < nh && rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);
   }
   __syncthreads();
-  if (tid < DW) {  // walk entering with offset L + tid
+  if (tid < dwin) {  // walk entering with offset L + tid
     int d = tid, bit = 0;
     bool ok = true;
     while (bit < WP) {
@@ -992,9 +1009,11 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
       const uint32_t m = masks[d * 32 + word] & (0xffffffffu << (bit & 31));
       if (!m) { bit = (word + 1) * 32; continue; }
       bit = word * 32 + __ffs(m);  // position after the rejection
-      if (++d >= DW + RX || d - tid >= RX) { ok = false; break; }
+      if (++d >= dwin + RX || d - tid >= RX) { ok = false; break; }
     }
     tables[w * DW + tid] = ok ? (uint8_t)(d - tid) : (uint8_t)255;
+  } else if (tid < DW) {
+    tables[w * DW + tid] = (uint8_t)255;  // outside this window's range
   }
 }
 
@@ -1551,11 +1570,11 @@ int encode_randk(const EncodeArgs& a, float* out) {
     const int64_t nwords = imin(n, k + k / 16 + 4096);
     const int64_t nwin = cdiv(nwords, WP);
     uint8_t* wsb = reinterpret_cast<uint8_t*>(p.w.list) + a16(4 * nwords);
-    double* expw = reinterpret_cast<double*>(wsb);
-    int64_t* Lw = reinterpret_cast<int64_t*>(wsb + a16(8 * nwin));
-    int64_t* tin = reinterpret_cast<int64_t*>(wsb + 2 * a16(8 * nwin));
-    WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + 3 * a16(8 * nwin));
-    uint8_t* tables = wsb + 3 * a16(8 * nwin) + 64;
+    double* expw = reinterpret_cast<double*>(wsb);  // [2][nwin]: expectation, variance
+    int64_t* Lw = reinterpret_cast<int64_t*>(wsb + a16(16 * nwin));
+    int64_t* tin = reinterpret_cast<int64_t*>(wsb + a16(16 * nwin) + a16(8 * nwin));
+    WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + a16(16 * nwin) + 2 * a16(8 * nwin));
+    uint8_t* tables = wsb + a16(16 * nwin) + 2 * a16(8 * nwin) + 64;
     // exact drift statistics of this (n, k) stream, once per group shape: sd of the total
     // rejections and the largest mean rejection count of a 1024-draw window
     const RandkStats rs = randk_stats(n, k, p.tail_shuffle != 0);
@@ -1571,7 +1590,8 @@ int encode_randk(const EncodeArgs& a, float* out) {
     int* comp = reinterpret_cast<int*>(tables + a16(nwin * DWr));           // [ngroups][DW]
     int* tg = comp + cdiv(nwin, CG) * DWr;                                   // [ngroups]
     note_launch(); k_randk_words<<<(unsigned)imax(1, imin(cdiv(nwords, 8 * 256), (int64_t)sm_count() * 4)), 256, 0, st>>>(p, p.w.list, nwords);
-    if (4 * n >= a16(4 * nwords) + 3 * a16(8 * nwin) + 64 + a16(nwin * DWr) + 4 * (cdiv(nwin, CG) * (DWr + 1))) {  // room for the parallel walk
+    if (4 * n >= a16(4 * nwords) + a16(16 * nwin) + 2 * a16(8 * nwin) + 64 + a16(nwin * DWr) +
+                     4 * (cdiv(nwin, CG) * (DWr + 1))) {  // room for the parallel walk
       const int64_t ngrp = cdiv(nwin, CG);
       note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
 #define MC_RANDK_WALK(DWV, RXV)                                                                                    \
@@ -1582,7 +1602,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
       MC_API_CHECK(cudaFuncSetAttribute(k_randk_tables<DWV, RXV>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts)); \
       cfg = true;                                                                                                 \
     }                                                                                                             \
-    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, expw, Lw, tables); \
+    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, expw, nwin, Lw, tables); \
     note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp);                      \
     note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, tg, tin, ctl);                   \
     note_launch(); k_randk_emit_draws<RXV><<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);           \
