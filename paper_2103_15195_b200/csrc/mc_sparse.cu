@@ -1023,69 +1023,86 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
 // groups (nwin / CG dependent lookups instead of nwin) and replays every group's windows
 // from its exact entering offset in parallel, writing tin[w].
 constexpr int CG = 16;
+// compose also records every intermediate entering offset: mid[w][e] = the offset window w
+// is entered with when its group is entered at L_g + e (-1 once the walk left the range), so
+// the replay below is one lookup per window, all windows in parallel
 template <int DW>
 __global__ void __launch_bounds__(DW) k_randk_compose(const int64_t* Lw, const uint8_t* tables, int64_t nwin,
-                                                      int* comp) {
+                                                      int* comp, int* mid) {
   const int64_t g = blockIdx.x, w0 = g * CG;
   int t = (int)Lw[w0] + (int)threadIdx.x;
   for (int64_t w = w0; w < imin(nwin, w0 + CG); ++w) {
+    mid[w * DW + threadIdx.x] = t;
+    if (t < 0) continue;
     const unsigned c = (unsigned)(t - (int)Lw[w]);
     const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
-    if (r == 255) { t = -1; break; }  // leaves the speculated range inside the group
-    t += r;
+    t = (r == 255) ? -1 : t + r;  // -1: left the speculated range inside the group
   }
   comp[g * DW + threadIdx.x] = t;
 }
 
 template <int DW>
 __global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, const uint8_t* tables, int64_t nwin,
-                                                      const int* comp, int* tg, int64_t* tin, WalkCtl* ctl) {
-  __shared__ int s_ng, s_fail_g;
-  __shared__ unsigned long long s_used;
+                                                      const int* comp, const int* mid, int* tg, int64_t* tin,
+                                                      WalkCtl* ctl) {
+  __shared__ int s_ng, s_texit;
+  __shared__ unsigned long long s_served, s_fail;
+  __shared__ int s_Lg[1024];  // group entry bases (ngrp <= 1024 keeps the serial loop on smem)
   const int64_t ngrp = cdiv(nwin, CG);
-  if (threadIdx.x == 0) {
-    ctl->fail_base = -1;
+  for (int64_t g = threadIdx.x; g < ngrp && g < 1024; g += blockDim.x) s_Lg[g] = (int)Lw[g * CG];
+  __syncthreads();
+  if (threadIdx.x == 0) {  // serial over groups: nwin / CG dependent lookups (one L2 load each)
     int t = 0;
     int64_t g = 0;
-    int fail_g = -1;
     for (; g < ngrp; ++g) {
       tg[g] = t;
-      const unsigned c = (unsigned)(t - (int)Lw[g * CG]);
+      const unsigned c = (unsigned)(t - (g < 1024 ? s_Lg[g] : (int)Lw[g * CG]));
       const int nt = c < (unsigned)DW ? comp[g * DW + c] : -1;
-      if (nt < 0) { fail_g = (int)g; ++g; break; }  // resolve inside this group below
+      if (nt < 0) { ++g; break; }  // the failure lies inside this group: found below
       t = nt;
     }
     s_ng = (int)g;  // groups with a known entering offset
-    s_fail_g = fail_g;
-    s_used = (unsigned long long)nwin;
+    s_texit = t;
+    s_served = s_fail = (unsigned long long)nwin;
   }
   __syncthreads();
-  // replay each group's windows from its entering offset: tin, the first window whose steps
-  // are all served (nwin_used) and, for the failing group, the hand-over to the serial walker
-  for (int64_t g = threadIdx.x; g < s_ng; g += blockDim.x) {
-    int t = tg[g];
-    for (int64_t w = g * CG; w < imin(nwin, (g + 1) * CG); ++w) {
-      if (w * WP - (int64_t)t >= p.k) { atomicMin(&s_used, (unsigned long long)w); break; }
-      const unsigned c = (unsigned)(t - (int)Lw[w]);
-      const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
-      if (r == 255) {  // only in the failing group: the serial walker continues from here
-        atomicMin(&s_used, (unsigned long long)w);
-        ctl->fail_base = w * WP;
-        ctl->fail_t0 = t;
-        break;
-      }
-      tin[w] = t;
-      t += r;
+  // every window of those groups in parallel: its entering offset, the first window whose
+  // steps are all served (nwin_used) and the first that leaves its range (serial hand-over)
+  const int64_t nw = imin(nwin, (int64_t)s_ng * CG);
+  for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) {
+    const int64_t g = w / CG, w0 = g * CG;
+    const unsigned e = (unsigned)(tg[g] - (int)Lw[w0]);
+    int t;
+    if (e < (unsigned)DW) {
+      t = mid[w * DW + e];
+      if (t < 0) continue;  // past this group's failing window
+    } else {
+      if (w != w0) continue;  // the group is entered outside its range: fails at its first window
+      t = tg[g];
     }
-    if (g == s_ng - 1 && s_fail_g < 0 && (g + 1) * CG >= nwin && nwin * WP - (int64_t)t < p.k) {
-      ctl->fail_base = nwin * WP;  // ran out of windows before every step was served
+    if (w * WP - (int64_t)t >= p.k) { atomicMin(&s_served, (unsigned long long)w); continue; }
+    const unsigned c = (unsigned)(t - (int)Lw[w]);
+    const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
+    if (r == 255) {  // at most one such window: the chain's first failure
+      atomicMin(&s_fail, (unsigned long long)w);
       ctl->fail_t0 = t;
+      continue;
     }
+    tin[w] = t;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    ctl->nwin_used = (int64_t)s_used;
-    if (ctl->fail_base >= 0 && ctl->fail_base / WP > (int64_t)s_used) ctl->fail_base = -1;  // served before
+    ctl->fail_base = -1;
+    if (s_fail < s_served) {
+      ctl->fail_base = (int64_t)s_fail * WP;
+      ctl->nwin_used = (int64_t)s_fail;
+    } else {
+      ctl->nwin_used = (int64_t)s_served;
+      if (s_served == (unsigned long long)nwin && nwin * WP - (int64_t)s_texit < p.k) {
+        ctl->fail_base = nwin * WP;  // ran out of windows before every step was served
+        ctl->fail_t0 = s_texit;
+      }
+    }
   }
 }
 
@@ -1589,9 +1606,10 @@ int encode_randk(const EncodeArgs& a, float* out) {
     const int RXr = tail(32) < 1e-6 ? 32 : tail(64) < 1e-6 ? 64 : 96;
     int* comp = reinterpret_cast<int*>(tables + a16(nwin * DWr));           // [ngroups][DW]
     int* tg = comp + cdiv(nwin, CG) * DWr;                                   // [ngroups]
+    int* mid = tg + cdiv(nwin, CG) + 4;                                      // [nwin][DW]
     note_launch(); k_randk_words<<<(unsigned)imax(1, imin(cdiv(nwords, 8 * 256), (int64_t)sm_count() * 4)), 256, 0, st>>>(p, p.w.list, nwords);
     if (4 * n >= a16(4 * nwords) + a16(16 * nwin) + 2 * a16(8 * nwin) + 64 + a16(nwin * DWr) +
-                     4 * (cdiv(nwin, CG) * (DWr + 1))) {  // room for the parallel walk
+                     4 * (cdiv(nwin, CG) * (DWr + 1) + 4 + nwin * DWr)) {  // room for the parallel walk
       const int64_t ngrp = cdiv(nwin, CG);
       note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
 #define MC_RANDK_WALK(DWV, RXV)                                                                                    \
@@ -1603,8 +1621,8 @@ int encode_randk(const EncodeArgs& a, float* out) {
       cfg = true;                                                                                                 \
     }                                                                                                             \
     note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, expw, nwin, Lw, tables); \
-    note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp);                      \
-    note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, tg, tin, ctl);                   \
+    note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp, mid);                 \
+    note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, mid, tg, tin, ctl);              \
     note_launch(); k_randk_emit_draws<RXV><<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);           \
   }
       if (DWr == 512 && RXr == 32) MC_RANDK_WALK(512, 32)
