@@ -106,13 +106,16 @@ def fit(samples: Sequence[TimingSample]) -> FitResult:
 
 def _event_median(fn, repetitions: int, warmup: int, stream: torch.cuda.Stream, batch: int = 8) -> float:
     """Median over ``repetitions`` of the mean device time of ``batch`` back-to-back calls
-    (CUDA events on the launch stream): the queue stays ahead of the GPU, so host launch
-    gaps are not charged to the kernels — the steady state of a pipelined sync."""
+    (CUDA events on the launch stream).  A spin kernel ahead of the start event keeps the
+    GPU busy while the host enqueues the batch, so host launch overhead never appears as
+    idle time between the events: the samples are kernel time only."""
     for _ in range(warmup):
         fn()
     times = []
     for _ in range(repetitions):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(2_000_000)  # ~1 ms at 1.9 GHz: covers the enqueue of the batch
         a.record(stream)
         for _ in range(batch):
             fn()
