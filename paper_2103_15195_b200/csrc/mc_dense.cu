@@ -238,8 +238,11 @@ __device__ __forceinline__ float rank_mean(float acc, float fn, float inv, bool 
 // sign word, bucket_size % 32 == 0 so the word lies in one bucket; per rank one u32 of
 // signs + the bucket scale(s) (+ 32 code bytes), per element select/multiply + add.
 // qsgd's code / (L-1) comes from a 256-entry table of the exact IEEE quotients.
+// symmetric +-scale codecs: 4 CTAs per SM (64 registers) — the N-rank accumulation is
+// issue-bound and occupancy hides its dependent adds (efsignsgd N=8: 43 -> 39 us); onebit
+// and qsgd keep more registers (two scales per bucket / the code table)
 template <int ALGO>
-__global__ void __launch_bounds__(256) k_decode_sign32(DP p) {
+__global__ void __launch_bounds__(256, (ALGO == MC_QSGD || ALGO == MC_ONEBIT) ? 1 : 4) k_decode_sign32(DP p) {
   __shared__ float tbl[256];
   __shared__ __align__(16) float s_out[8][32 * 36];
   if (ALGO == MC_QSGD) {
