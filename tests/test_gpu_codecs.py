@@ -164,3 +164,42 @@ def test_signsgd_large_group_scale_matches_numpy(n, C):
     want = np.float32(np.abs(x).mean())
     assert np.asarray(h.values).view(np.uint32)[0] == np.asarray([want]).view(np.uint32)[0]
     assert np.array_equal(np.asarray(h.bits), np.packbits(x >= 0))
+
+
+@pytest.mark.parametrize("algo,ef", [("qsgd", False), ("qsgd", True), ("terngrad", False), ("int8", False),
+                                     ("int8", True)])
+def test_quantizer_scale_range_matches_oracle(algo, ef, C):
+    """The quantizers divide by the bucket scale with the reciprocal hoisted per bucket and
+    the IEEE fast path inline; elements or scales outside [2^-40, 2^40] take the full
+    division.  Magnitudes from 2^-70 to 2^60, whole buckets of tiny / huge values and
+    exact zeros: codes, scales and residuals bit-exact against the oracle."""
+    import torch
+
+    import mergecomp_oracle as O
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    rng = np.random.default_rng(2103)
+    n = 512 * 400 + 77
+    e = rng.uniform(-70, 20, n)
+    g = (np.sign(rng.standard_normal(n)) * rng.uniform(1, 2, n) * np.exp2(e)).astype(np.float32)
+    g[512 * 3:512 * 4] = (rng.standard_normal(512) * 2.0 ** -50).astype(np.float32)  # scale < 2^-40
+    g[512 * 7:512 * 8] = (rng.standard_normal(512) * 2.0 ** 55).astype(np.float32)   # scale > 2^40
+    g[512 * 9:512 * 10] = 0.0
+    g[rng.integers(0, n, 500)] = 0.0
+    g[rng.integers(0, n, 200)] = -0.0
+    spec = CompressorSpec(algo, error_feedback=ef, bucket_size=512)
+    st_d, st_r = None, None
+    for t in range(2):
+        seed = O.derive_seed(11, 0, t, 0)
+        p_dev, st_d = C.encode(spec, torch.from_numpy(g).cuda(), st_d, seed=seed)
+        p_ref, st_r = O.encode(spec, g, st_r, seed=seed)
+        d = p_dev.to_host()
+        for name in ("values", "bits"):
+            a, b = getattr(d, name), getattr(p_ref, name)
+            if b is None:
+                assert a is None or len(a) == 0
+            else:
+                _eq_bits(np.asarray(a), np.asarray(b), f"{algo} t{t} {name}")
+        if ef:
+            _eq_bits(st_d.residual.cpu().numpy(), np.asarray(st_r.residual), f"{algo} t{t} residual")
+        _eq_bits(C.aggregate(spec, [p_dev]).cpu().numpy(), np.asarray(O.aggregate(spec, [p_ref])), f"{algo} t{t} mean")
