@@ -38,21 +38,71 @@ struct SP {
 // pairwise pass reads at once, ~n/4 apart, fall into disjoint bank octets; float4 aligned
 __device__ __forceinline__ int spos(int q) { return q + 8 * (q >> 5); }
 
-// Streams node `node` (depth D) once; returns the node's pairwise sum (all lanes).
+// warp_pairwise_small over the spos() layout with the leaf reads addressed from four
+// per-lane bases: lane j of a leaf group reads q = o + 8t (o = leaf offset + j, leaf offsets
+// are multiples of 8), whose padded position is spos(o) + 8t + 8*((k + t) >> 2) with
+// k = (o >> 3) & 3; for t = 4u + r that is B_r + 8t + 8u, B_r = spos(o) + 8*((k + r) >> 2),
+// so every unrolled read is one LDS with an immediate offset.  Same sums, same order.
+template <int D>
+__device__ __forceinline__ float node_pairwise(const float* a, int L) {
+  const int lane = threadIdx.x & 31;
+  if (L < 8) {
+    float s = -0.0f;
+    if (lane == 0)
+      for (int q = 0; q < L; ++q) s = __fadd_rn(s, a[spos(q)]);
+    return __shfl_sync(FULL, s, 0);
+  }
+  int nleaf = 0, my_off = 0, my_len = 0;
+  pw::collect<D>(0, L, nleaf, my_off, my_len);
+  float leafv = 0.0f;
+  for (int base = 0; base < nleaf; base += 4) {
+    const int g = lane >> 3, j = lane & 7, leaf = base + g;
+    const int off = __shfl_sync(FULL, my_off, leaf & 31), len = __shfl_sync(FULL, my_len, leaf & 31);
+    const bool act = leaf < nleaf;
+    const int body = act ? len - (len % 8) : 0;
+    const int o = off + j, k = (o >> 3) & 3;
+    const float* B[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) B[r] = a + spos(o) + 8 * ((k + r) >> 2);
+    float v = act ? B[0][0] : 0.0f;
+#pragma unroll
+    for (int t = 1; t < 16; ++t)
+      if (8 * t < body) v = __fadd_rn(v, B[t & 3][8 * t + 8 * (t >> 2)]);
+    v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 1));
+    v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 2));
+    v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 4));
+    if (act && j == 0)
+      for (int q = body; q < len; ++q) v = __fadd_rn(v, a[spos(off + q)]);
+#pragma unroll
+    for (int gg = 0; gg < 4; ++gg) {
+      const float w = __shfl_sync(FULL, v, 8 * gg);
+      if (lane == base + gg) leafv = w;
+    }
+  }
+  int cnt = 0;
+  return pw::combine<D>(L, cnt, leafv);
+}
+
+// Streams the depth-D node [off, off + len) once; returns its pairwise sum (all lanes).
 // Nodes start at multiples of 8 elements (so at sign-byte boundaries and 32-byte
 // aligned) and hold <= 128*NCH elements: every lane issues all of its float4 loads of a
 // group of 4 chunks before it touches any of them (one HBM round trip per group, not one
 // per 32 elements), then writes sign bytes, the signum momentum, and |c32| to smem.
 // MOM / EF are compile-time so the common signsgd node is a lean load/compare/store loop.
-template <int NCH, bool MOM, bool EF, bool VEC>
-__device__ __forceinline__ float sign_node(const SP& p, int node, float* a) {
-  const int lane = threadIdx.x & 31;
-  int off = 0, len = (int)p.n;  // groups are < 2^31 elements (NODE_MAX check at launch)
-  for (int d = p.D - 1; d >= 0; --d) {  // bit d of the node index = right child at that level
-    const int m = (len >> 1) & ~7;      // n2 = n/2 - (n/2) % 8
-    if ((node >> d) & 1) { off += m; len -= m; }
+// Descends `levels` levels of the numpy split rule from the node [off, len): bit d of
+// `path` = right child at the d-th level from the bottom.
+__device__ __forceinline__ void split_descend(int path, int levels, int& off, int& len) {
+  for (int d = levels - 1; d >= 0; --d) {
+    const int m = (len >> 1) & ~7;  // n2 = n/2 - (n/2) % 8
+    if ((path >> d) & 1) { off += m; len -= m; }
     else len = m;
   }
+}
+
+// `off`, `len`: the node's position (groups are < 2^31 elements; NODE_MAX check at launch)
+template <int NCH, bool MOM, bool EF, bool VEC>
+__device__ __forceinline__ float sign_node(const SP& p, int off, int len, float* a) {
+  const int lane = threadIdx.x & 31;
   const int L = len;
   const float* g = p.pro.g + off;
   float* mo = MOM ? p.pro.m + off : nullptr;
@@ -133,10 +183,9 @@ __device__ __forceinline__ float sign_node(const SP& p, int node, float* a) {
   __syncwarp();
   // levels above the leaves (<= 128 elements): a split leaves children <= len/2 + 7.5, so
   // after d splits a node is <= L/2^d + 15; depth 3 holds up to L = 904, 4 up to 1808
-  auto get = [&](int q) { return a[spos(q)]; };
-  if (NCH <= 4 || L <= 904) return warp_pairwise_small<3>(get, L);
-  if (NCH <= 8 || L <= 1808) return warp_pairwise_small<4>(get, L);
-  return warp_pairwise_small<5>(get, L);
+  if (NCH <= 4 || L <= 904) return node_pairwise<3>(a, L);
+  if (NCH <= 8 || L <= 1808) return node_pairwise<4>(a, L);
+  return node_pairwise<5>(a, L);
 }
 
 template <int NCH, bool MOM, bool EF, bool VEC>
@@ -145,8 +194,18 @@ __global__ void __launch_bounds__(SW * 32) k_sign_nodes(SP p) {
   float(*sm)[160 * NCH] = reinterpret_cast<float(*)[160 * NCH]>(sm_dyn);
   __shared__ float s_node[SW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
-  const float s = sign_node<NCH, MOM, EF, VEC>(p, (int)blockIdx.x * SW + warp, sm[warp]);
+  __shared__ int s_root[2];
+  if (threadIdx.x == 0) {  // the CTA's 8 nodes share the top D-3 levels of the descent
+    if (blockIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
+    int off = 0, len = (int)p.n;
+    split_descend((int)blockIdx.x, p.D - 3, off, len);
+    s_root[0] = off;
+    s_root[1] = len;
+  }
+  __syncthreads();
+  int off = s_root[0], len = s_root[1];
+  split_descend(warp, 3, off, len);
+  const float s = sign_node<NCH, MOM, EF, VEC>(p, off, len, sm[warp]);
   if (lane == 0) s_node[warp] = s;
   __syncthreads();
   if (threadIdx.x == 0) {  // nodes 8b .. 8b+7 form a perfect subtree (3 levels)
@@ -161,7 +220,9 @@ template <bool MOM, bool EF>
 __global__ void k_sign_nodes_small(SP p) {
   __shared__ __align__(16) float sm[160 * 16];
   if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
-  const float s = sign_node<16, MOM, EF, false>(p, blockIdx.x, sm);
+  int off = 0, len = (int)p.n;
+  split_descend((int)blockIdx.x, p.D, off, len);
+  const float s = sign_node<16, MOM, EF, false>(p, off, len, sm);
   if (threadIdx.x == 0) p.partial[blockIdx.x] = s;
 }
 
