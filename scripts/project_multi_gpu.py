@@ -18,20 +18,24 @@ from paper_2103_15195_b200 import compressors as C, gradsets  # noqa: E402
 from paper_2103_15195_b200.spec import CompressorSpec  # noqa: E402
 
 
-def timed(fn, reps=20):
+def timed(fn, reps=20, trials=3):
     """Device time per call: a ~5 ms spin kernel keeps the GPU busy while the host enqueues
-    all reps, so host launch overhead never shows up as GPU idle time between the events."""
+    all reps, so host launch overhead never shows up as GPU idle time between the events.
+    Minimum over `trials` (a host stall longer than the spin would leave the GPU idle)."""
     for _ in range(3):
         fn()
-    torch.cuda.synchronize()
-    torch.cuda._sleep(10_000_000)
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(reps):
-        fn()
-    e.record()
-    e.synchronize()
-    return s.elapsed_time(e) / reps
+    best = float("inf")
+    for _ in range(trials):
+        torch.cuda.synchronize()
+        torch.cuda._sleep(10_000_000)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e) / reps)
+    return best
 
 
 def main():
