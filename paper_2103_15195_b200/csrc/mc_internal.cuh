@@ -202,6 +202,53 @@ __device__ __forceinline__ float warp_pairwise_small(const Get& get, int L) {
   return pw::combine<D>(L, cnt, leafv);
 }
 
+__device__ __forceinline__ int pad32(int q) { return q + 8 * (q >> 5); }
+
+// warp_pairwise_small over the pad32() layout (q + 8 * (q >> 5)) with the leaf reads addressed from four
+// per-lane bases: lane j of a leaf group reads q = o + 8t (o = leaf offset + j, leaf offsets
+// are multiples of 8), whose padded position is pad32(o) + 8t + 8*((k + t) >> 2) with
+// k = (o >> 3) & 3; for t = 4u + r that is B_r + 8t + 8u, B_r = pad32(o) + 8*((k + r) >> 2),
+// so every unrolled read is one LDS with an immediate offset.  Same sums, same order.
+template <int D>
+__device__ __forceinline__ float pairwise_pad32(const float* a, int L) {
+  const int lane = threadIdx.x & 31;
+  if (L < 8) {
+    float s = -0.0f;
+    if (lane == 0)
+      for (int q = 0; q < L; ++q) s = __fadd_rn(s, a[pad32(q)]);
+    return __shfl_sync(FULL, s, 0);
+  }
+  int nleaf = 0, my_off = 0, my_len = 0;
+  pw::collect<D>(0, L, nleaf, my_off, my_len);
+  float leafv = 0.0f;
+  for (int base = 0; base < nleaf; base += 4) {
+    const int g = lane >> 3, j = lane & 7, leaf = base + g;
+    const int off = __shfl_sync(FULL, my_off, leaf & 31), len = __shfl_sync(FULL, my_len, leaf & 31);
+    const bool act = leaf < nleaf;
+    const int body = act ? len - (len % 8) : 0;
+    const int o = off + j, k = (o >> 3) & 3;
+    const float* B[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) B[r] = a + pad32(o) + 8 * ((k + r) >> 2);
+    float v = act ? B[0][0] : 0.0f;
+#pragma unroll
+    for (int t = 1; t < 16; ++t)
+      if (8 * t < body) v = __fadd_rn(v, B[t & 3][8 * t + 8 * (t >> 2)]);
+    v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 1));
+    v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 2));
+    v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 4));
+    if (act && j == 0)
+      for (int q = body; q < len; ++q) v = __fadd_rn(v, a[pad32(off + q)]);
+#pragma unroll
+    for (int gg = 0; gg < 4; ++gg) {
+      const float w = __shfl_sync(FULL, v, 8 * gg);
+      if (lane == base + gg) leafv = w;
+    }
+  }
+  int cnt = 0;
+  return pw::combine<D>(L, cnt, leafv);
+}
+
 // numpy float32 mean of a sequence with a known pairwise sum:  f32( f64(0 + P) / n ).
 __device__ __forceinline__ float np_mean(float pairwise_sum, int64_t n) {
   const float s = __fadd_rn(0.0f, pairwise_sum);
