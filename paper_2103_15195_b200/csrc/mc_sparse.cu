@@ -340,9 +340,7 @@ __device__ __forceinline__ uint64_t cta_chunk_prefix(uint64_t warp_total, uint64
 // look-back chain over 12K tiles costs more than the whole read).  Only 128-element chunks
 // whose pass-1 maximum reaches bin B1 are read at all.
 __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
-  __shared__ uint32_t h2[NB2];
   __shared__ uint32_t s_wt[8];
-  for (int i = threadIdx.x; i < NB2; i += blockDim.x) h2[i] = 0;
   const uint32_t B1 = p.w.ctl[CTL_B1], thr = B1 << S1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bid = blockIdx.x;
@@ -374,7 +372,6 @@ __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
         if (e0 + q < p.n) kk[i][q] = key_at(p, e0 + q);
     }
   }
-  __syncthreads();  // h2 zeroed
   uint32_t keep = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -384,7 +381,8 @@ __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
       const uint32_t key = kk[i][q] & 0x7fffffffu;
       const bool in = c0 + 128 * i + 4 * lane + q < p.n;
       keep |= (uint32_t)(in && key >= thr) << (4 * i + q);
-      if (in && (key >> S1) == B1) atomicAdd(&h2[(key >> S2) & (NB2 - 1)], 1u);
+      // the few keys inside bin B1 go straight to the L2 histogram (no per-tile smem copy)
+      if (in && (key >> S1) == B1) atomicAdd(&p.w.hist[NB1 + ((key >> S2) & (NB2 - 1))], 1u);
     }
   }
   const uint32_t wtot = __reduce_add_sync(FULL, __popc(keep));
@@ -409,8 +407,6 @@ __global__ void __launch_bounds__(256) k_topk_pass2(TP p) {
     }
   }
   if (threadIdx.x == 0) p.w.segcnt[bid] = tot;
-  for (int i = threadIdx.x; i < NB2; i += blockDim.x)
-    if (h2[i]) atomicAdd(&p.w.hist[NB1 + i], h2[i]);
 }
 
 // hist3: every CTA turns the pass-2 tile counts into their exclusive prefix in shared
