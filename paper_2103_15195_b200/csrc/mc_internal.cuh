@@ -62,7 +62,8 @@ struct Ctx {
 
 // --------------------------------------------------------------------------------------------
 // Philox4x64-10, counter = (block + 1, 0, 0, 0): numpy's Philox bit generator
-// (Random123 round function).  Uniform double = (w >> 11) * 2^-53.
+// (Random123 round function).  Uniform double = (w >> 11) * 2^-53
+// (compared without forming it: u53_below in mc_bucket.cu).
 struct Philox {
   uint64_t k0, k1;
   __device__ __forceinline__ void block(uint64_t blk, uint64_t out[4]) const {
@@ -79,7 +80,6 @@ struct Philox {
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
   }
 };
-__device__ __forceinline__ double u53(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
 
 // --------------------------------------------------------------------------------------------
 // numpy float32 pairwise summation (umath loops_utils pairwise_sum):
