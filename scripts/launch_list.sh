@@ -17,7 +17,11 @@ for r in rows:
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r)); k = d["Kernel Name"].split("(")[0].replace("void mc::<unnamed>::", "")
         agg.setdefault(k, []).append(float(d["Metric Value"].replace(",","")))
+# the e2e leg launches the fused kernels per 8 MB chunk: report the whole-group launches
+# (>= half the longest) separately from the mean over all launches
 for k, v in agg.items():
-    print(f"  {k[:60]:60s} n={len(v):3d} mean={sum(v)/len(v)/1000:8.1f} us")
+    big = [x for x in v if x >= 0.5 * max(v)]
+    print(f"  {k[:60]:60s} n={len(v):3d} mean={sum(v)/len(v)/1000:8.1f} us"
+          f"  whole-group n={len(big):3d} mean={sum(big)/len(big)/1000:8.1f} us")
 PY
 done
