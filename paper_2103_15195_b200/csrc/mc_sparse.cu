@@ -17,8 +17,6 @@ namespace mc {
 namespace {
 
 constexpr int TB = 256;         // threads per compaction block
-constexpr int ITEMS = 16;       // consecutive elements per thread
-constexpr int TILE = TB * ITEMS;
 
 // ------------------------------------------------------------------ workspace layout
 // top-k radix select over the 31-bit magnitude key: 11 / 11 / 9 bits (a 12-bit first
@@ -1258,7 +1256,6 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
       m &= m - 1;
       const int64_t e = (w0 + q) * 32 + b;
       float c32;
-      bool bad = false;
       double c;
       if (p.pro.r) {
         c = p.pro.r[e];  // pass 1 stored r <- c
@@ -1267,7 +1264,6 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
         c32 = p.pro.m ? p.pro.m[e] : p.pro.g[e];
         c = (double)c32;
       }
-      (void)bad;
       const float v = p.unbiased ? __fmul_rn(c32, p.scale) : c32;
       p.idx_out[pos] = (uint32_t)e;
       p.val_out[pos] = v;
