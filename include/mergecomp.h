@@ -20,6 +20,7 @@
  *   mc_decode_mean        <- aggregate (+ decode)   compressors.py:519-532, 427-516
  *   mc_pack / mc_unpack   <- Trainer._group_slices  trainer.py:344-348 (merge stage)
  *   mc_serialize          <- serialize              compressors.py:601-620
+ *   mc_deserialize        <- deserialize            compressors.py:623-645
  */
 #ifndef MERGECOMP_H
 #define MERGECOMP_H
@@ -44,7 +45,10 @@ extern "C" {
 #define MC_ERR_INDEX_RANGE 0x2u  /* "corrupt payload: index out of range"   compressors.py:444 */
 #define MC_ERR_INDEX_ORDER 0x4u  /* "corrupt payload: indices not increasing" compressors.py:445 */
 #define MC_ERR_HEADER 0x8u       /* payload header does not match spec / length */
-#define MC_ERR_PEER_TIMEOUT 0x10u /* mc_push_wait: a peer's payload did not arrive (~10 s) */
+#define MC_ERR_PEER_TIMEOUT 0x10u /* mc_push_wait: a peer's payload did not arrive in time (then traps) */
+
+/* mc_push_wait timeout when the caller passes 0: 600 s, the order of NCCL's collective timeout */
+#define MC_PUSH_TIMEOUT_DEFAULT_NS 600000000000ull
 
 /* algorithm ids == position in the reference ALGORITHMS tuple (compressors.py:29-43) */
 enum {
@@ -144,6 +148,14 @@ int mc_unpack(const float* fused, float* const* dsts, const int64_t* numels, int
 int mc_serialize(const mc_spec* spec, const void* payload, int64_t n, void* out, int64_t out_cap,
                  int64_t* out_len, void* stream);
 
+/* Inverse of mc_serialize: canonical bytes `data` (device, `len` bytes) -> aligned device
+ * payload (capacity payload_cap bytes; sparsifiers get cap = n_idx).  Validates exactly as
+ * deserialize() does (short buffer, unknown algorithm id, length vs header) plus the header
+ * against `spec` and its layout; *n_out (host) = original_len.  Reads the 22-byte header
+ * synchronously (the section sizes depend on it). */
+int mc_deserialize(const mc_spec* spec, const void* data, int64_t len, void* payload, int64_t payload_cap,
+                   int64_t* n_out, void* stream);
+
 /* Encode fused with the allgather over peer memory (NVLink P2P / symmetric memory): the
  * payload is written to `payload` (this rank's slot of its own gather buffer) and to every
  * dsts[j] (this rank's slot in rank j's gather buffer; host array of nranks device / peer-
@@ -152,12 +164,15 @@ int mc_serialize(const mc_spec* spec, const void* payload, int64_t n, void* out,
  * pipe-kernel codecs (efsignsgd, onebit, int8) store into the peer slots from the encode
  * kernel itself; the others encode, then copy.  mc_push_wait: the stream waits until the
  * local flags[0..nranks) all equal epoch — the gathered payloads are then complete in rank
- * order, exactly what mc_decode_mean reads (replaces the NCCL allgather of trainer.py:377-389). */
+ * order, exactly what mc_decode_mean reads (replaces the NCCL allgather of trainer.py:377-389).
+ * A peer silent for timeout_ns (0 = MC_PUSH_TIMEOUT_DEFAULT_NS) sets MC_ERR_PEER_TIMEOUT and
+ * traps: the stream's context faults, nothing after the wait (the decode) runs. */
 int mc_encode_push(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
                    uint64_t key_lo, uint64_t key_hi, void* payload, void* const* dsts, uint32_t* const* flags,
                    int32_t nranks, uint32_t epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
                    void* stream);
-int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint32_t* err_flags, void* stream);
+int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,
+                 void* stream);
 
 /* Host-buffer sync of one rank (world size 1), enqueued natively: the trainer's step on a
  * worker's host gradient (trainer.py:360-395, one worker).  For each group: H2D of

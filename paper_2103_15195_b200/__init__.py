@@ -11,13 +11,24 @@ from .spec import ALGORITHMS, CompressorSpec, payload_bytes, top_k_count  # noqa
 from .profiles import LayerProfile, ModelProfile, Partition  # noqa: F401
 
 
-def __getattr__(name):  # lazy: importing the package never needs a GPU
-    if name in ("CompressedPayload", "ResidualState"):
-        from . import compressors
+# The reference package root re-exports (mergesched/__init__.py:20-43), resolved lazily so
+# importing the package stays cheap.  TrainConfig / TrainReport belong to the reference's
+# convergence trainer (trainer.py:47-229), which is out of scope.
+_LAZY = {
+    "CompressedPayload": "compressors", "ResidualState": "compressors",
+    "CostParams": "costmodel", "TimingSample": "costmodel",
+    "SimConfig": "simulator", "SimReport": "simulator",
+    "SearchConfig": "scheduler", "SearchResult": "scheduler",
+}
 
-        return getattr(compressors, name)
-    if name in ("SearchConfig", "SearchResult"):
-        from . import scheduler
+__all__ = ["__version__", "ALGORITHMS", "CompressorSpec", "payload_bytes", "top_k_count", "LayerProfile",
+           "ModelProfile", "Partition", *_LAZY]
 
-        return getattr(scheduler, name)
-    raise AttributeError(name)
+
+def __getattr__(name):
+    mod = _LAZY.get(name)
+    if mod is None:
+        raise AttributeError(name)
+    import importlib
+
+    return getattr(importlib.import_module(f".{mod}", __name__), name)

@@ -64,10 +64,12 @@ _SIGS = {
     "mc_pack": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P, _P]),
     "mc_unpack": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P]),
     "mc_serialize": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), _P]),
+    "mc_deserialize": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                      _P]),
     "mc_encode_push": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, ctypes.c_uint64, ctypes.c_uint64, _P,
                                       ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_uint32, _P,
                                       ctypes.c_int64, _P, _P]),
-    "mc_push_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P]),
+    "mc_push_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, _P, _P]),
     "mc_pipe_create": (ctypes.c_int, [ctypes.POINTER(_P)]),
     "mc_pipe_destroy": (None, [_P]),
     "mc_pipe_group": (ctypes.c_int, [_P, _SPEC, _P, _P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, ctypes.c_uint64,

@@ -48,6 +48,7 @@ __all__ = [
     "ALGORITHMS", "HEADER_BYTES", "CompressorSpec", "ResidualState", "CompressedPayload", "DevicePayload",
     "encode", "decode", "aggregate", "payload_bytes", "serialize", "deserialize", "derive_seed",
     "top_k_count", "empirical_error_bound", "device_encode", "device_encode_decode", "device_decode_mean",
+    "device_deserialize",
 ]
 
 _HDR_DEV = 32  # sizeof(mc_payload_header)
@@ -170,16 +171,22 @@ class CompressedPayload:
 # ------------------------------------------------------------------ device plumbing
 
 class _Workspace:
-    """One growable scratch buffer per device (the library keeps no state)."""
+    """Growable scratch buffers keyed by (device, stream): the library keeps no state, and two
+    encodes in flight on different streams (e.g. two GradSync side streams) never share
+    scratch (tile tickets, look-back status, push counters).  Each buffer is allocated on its
+    own stream, so replacing a smaller one is stream-ordered by the caching allocator."""
 
     def __init__(self):
-        self._bufs: dict[int, torch.Tensor] = {}
+        self._bufs: dict[tuple[int, int], torch.Tensor] = {}
 
-    def get(self, device: torch.device, nbytes: int) -> torch.Tensor:
-        key = device.index if device.index is not None else torch.cuda.current_device()
+    def get(self, device: torch.device, nbytes: int, stream=None) -> torch.Tensor:
+        dev = device.index if device.index is not None else torch.cuda.current_device()
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        key = (dev, st.cuda_stream)
         buf = self._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            with torch.cuda.stream(st):
+                buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
             self._bufs[key] = buf
         return buf
 
@@ -218,7 +225,7 @@ def device_encode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[t
     if out is None:
         out = torch.empty(L.bytes, dtype=torch.uint8, device=grad.device)
     wsb = _native.workspace_bytes(cs, n)
-    ws = _WS.get(grad.device, wsb)
+    ws = _WS.get(grad.device, wsb, stream)
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=grad.device)
     lo, hi = split_seed(seed)
@@ -241,7 +248,7 @@ def device_encode_decode(spec: CompressorSpec, grad: torch.Tensor, residual: Opt
     L = _native.layout(cs, n)
     if payload is None:
         payload = torch.empty(L.bytes, dtype=torch.uint8, device=grad.device)
-    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n))
+    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n), stream)
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=grad.device)
     lo, hi = split_seed(seed)
@@ -264,7 +271,7 @@ def device_encode_push(spec: CompressorSpec, grad: torch.Tensor, residual: Optio
     fused with the encode (mc_encode_push).  Pair with ``push_wait`` before decoding."""
     n = grad.numel()
     cs = cspec if cspec is not None else spec.to_c()
-    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n))
+    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n), stream)
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=grad.device)
     lo, hi = split_seed(seed)
@@ -279,13 +286,16 @@ def device_encode_push(spec: CompressorSpec, grad: torch.Tensor, residual: Optio
     )
 
 
-def push_wait(flags: torch.Tensor, nranks: int, epoch: int, err: Optional[torch.Tensor] = None, stream=None) -> None:
-    """The stream waits until all ``nranks`` local flag words equal ``epoch`` (mc_push_wait);
-    a peer silent for ~10 s sets MC_ERR_PEER_TIMEOUT in ``err`` instead of hanging."""
+def push_wait(flags: torch.Tensor, nranks: int, epoch: int, err: Optional[torch.Tensor] = None, stream=None,
+              timeout_s: float = 0.0) -> None:
+    """The stream waits until all ``nranks`` local flag words equal ``epoch`` (mc_push_wait).
+    A peer silent for ``timeout_s`` (0: the library default, 600 s) sets MC_ERR_PEER_TIMEOUT
+    and traps — the job fails loudly instead of decoding stale slots."""
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=flags.device)
-    _native.check(_native.lib().mc_push_wait(flags.data_ptr(), nranks, int(epoch) & 0xFFFFFFFF, err.data_ptr(),
-                                             _stream_ptr(stream)), "mc_push_wait")
+    _native.check(_native.lib().mc_push_wait(flags.data_ptr(), nranks, int(epoch) & 0xFFFFFFFF,
+                                             int(timeout_s * 1e9), err.data_ptr(), _stream_ptr(stream)),
+                  "mc_push_wait")
 
 
 def device_decode_mean(spec: CompressorSpec, base: torch.Tensor, stride: int, nranks: int, n: int,
@@ -443,8 +453,12 @@ def encode(spec: CompressorSpec, gradient, state: Optional[ResidualState] = None
     def to_dev(a, dtype):
         if a is None:
             return None
-        if isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == dtype and a.is_contiguous():
-            return a if on_dev else a.clone()
+        if isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == dtype:
+            # a private copy: the reference returns NEW state objects and raises on a
+            # non-finite gradient before touching state (compressors.py:384-411), so the
+            # caller's tensors are never updated in place (the sync engine, which owns its
+            # state, uses device_encode directly)
+            return a.contiguous().clone()
         return torch.as_tensor(np.asarray(a) if not isinstance(a, torch.Tensor) else a, dtype=dtype).to(dev).contiguous()
 
     r = to_dev(state.residual, torch.float64) if (state is not None and use_ef) else None
@@ -580,3 +594,42 @@ def deserialize(data: bytes) -> CompressedPayload:
     if algo in SPARSIFIERS and indices is None:
         indices = np.empty(0, dtype="<u4")
     return CompressedPayload(algo, original_len, indices, values, bits, flags)
+
+
+def device_deserialize(spec: CompressorSpec, data) -> CompressedPayload:
+    """Canonical bytes (``bytes`` or a CUDA uint8 tensor) -> device payload (mc_deserialize,
+    the on-device inverse of ``serialize``; compressors.py:623-645).  Raises the reference's
+    ``ValueError`` messages on malformed input."""
+    dev = data.device if isinstance(data, torch.Tensor) else _device()
+    if not isinstance(data, torch.Tensor):
+        raw = np.frombuffer(bytes(data), np.uint8)
+        if raw.size < HEADER_BYTES:
+            raise ValueError("payload shorter than header")
+        data = torch.from_numpy(raw.copy()).to(dev)
+    if data.numel() < HEADER_BYTES:
+        raise ValueError("payload shorter than header")
+    hdr = data[:HEADER_BYTES].cpu().numpy().tobytes()
+    _, _, n, n_idx, _, _ = struct.unpack_from("<BBQIII", hdr)
+    cs = spec.to_c()
+    cap = n_idx if spec.algorithm in SPARSIFIERS else 0
+    try:
+        L = _native.layout(cs, max(int(n), 1), max(cap, 1) if spec.algorithm == "threshold" else 0)
+    except _native.NativeError as e:
+        raise ValueError(f"corrupt payload: {e}") from None
+    nbytes = max(L.bytes, 32 + 2 * _a16(4 * cap)) if spec.algorithm in SPARSIFIERS else L.bytes
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    n_out = ctypes.c_int64()
+    st = _native.lib().mc_deserialize(ctypes.byref(cs), data.data_ptr(), data.numel(), buf.data_ptr(), buf.numel(),
+                                      ctypes.byref(n_out), _stream_ptr())
+    if st != _native.MC_OK:
+        raise ValueError(_native.lib().mc_last_error().decode(errors="replace"))
+    L2 = _native.layout(cs, int(n), max(cap, 1) if spec.algorithm == "threshold" else 0)
+    if spec.algorithm in SPARSIFIERS:
+        L2.cap = cap
+        L2.n_val = cap
+        L2.off_val = 32 + _a16(4 * cap)
+        L2.off_bits = L2.off_codes = L2.bytes = L2.off_val + _a16(4 * cap)
+    dp = DevicePayload(spec, int(n), buf, L2, cap=cap if spec.algorithm in SPARSIFIERS else None)
+    if spec.algorithm in SPARSIFIERS:
+        dp._count = cap
+    return _payload_from_device(spec, dp, host=False)

@@ -291,8 +291,10 @@ __global__ void __launch_bounds__(256) k_push_copy(PushArgs a) {
   }
 }
 // Wait (one CTA) until every flag equals the epoch: the gathered payloads are complete.
-// Bounded (~10 s): a peer that never signals raises MC_ERR_PEER_TIMEOUT instead of hanging.
-__global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch, uint32_t* err) {
+// Bounded: a peer silent for timeout_ns sets MC_ERR_PEER_TIMEOUT and TRAPS — the context
+// faults and the job fails loudly (like NCCL's watchdog abort) instead of decoding stale or
+// half-written slots and losing the double-buffer invariant.
+__global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch, uint64_t timeout_ns, uint32_t* err) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     uint64_t t0 = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -300,7 +302,11 @@ __global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch, uint32
       __nanosleep(256);
       uint64_t t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 10000000000ull) { atomicOr(err, MC_ERR_PEER_TIMEOUT); break; }
+      if (t - t0 > timeout_ns) {
+        atomicOr(err, MC_ERR_PEER_TIMEOUT);
+        __threadfence_system();
+        __trap();
+      }
     }
   }
   __syncthreads();
@@ -351,10 +357,12 @@ int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* resid
   return launch_push_copy(static_cast<const uint8_t*>(payload), L.bytes, a, static_cast<cudaStream_t>(stream));
 }
 
-int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint32_t* err_flags, void* stream) {
+int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,
+                 void* stream) {
   if (!flags || nranks < 1 || !err_flags) { set_error("bad flags"); return MC_EINVAL; }
+  if (timeout_ns == 0) timeout_ns = MC_PUSH_TIMEOUT_DEFAULT_NS;
   note_launch();
-  k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, epoch, err_flags);
+  k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, epoch, timeout_ns, err_flags);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
@@ -467,6 +475,28 @@ __global__ void k_serialize(SerArgs a) {
   }
 }
 
+// Inverse of k_serialize: canonical bytes (22-byte header + packed sections) -> the
+// aligned device layout; thread 0..31 write the 32-byte mc_payload_header.
+struct DeserArgs {
+  mc_payload_header h;
+  const uint8_t* in;
+  uint8_t* dst[4];
+  int64_t len[4];
+  int64_t start[5];  // input offsets of the 4 sections (start[0] = 22)
+  uint8_t* payload;
+};
+
+__global__ void k_deserialize(DeserArgs a) {
+  const int64_t total = a.start[4];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid < (int64_t)sizeof(mc_payload_header)) a.payload[tid] = reinterpret_cast<const uint8_t*>(&a.h)[tid];
+  for (int64_t o = 22 + tid; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    int s = 0;
+    while (s < 3 && o >= a.start[s + 1]) ++s;
+    a.dst[s][o - a.start[s]] = a.in[o];
+  }
+}
+
 }  // namespace
 }  // namespace mc
 
@@ -523,6 +553,79 @@ int mc_serialize(const mc_spec* s, const void* payload, int64_t n, void* out, in
   if (out_cap < a.start[4]) { set_error("serialize buffer too small (%lld < %lld)", (long long)out_cap, (long long)a.start[4]); return MC_EINVAL; }
   const unsigned grid = (unsigned)imax(1, imin(cdiv(a.start[4], 256), 4096));
   note_launch(); k_serialize<<<grid, 256, 0, st>>>(a);
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+
+int mc_deserialize(const mc_spec* s, const void* data, int64_t len, void* payload, int64_t payload_cap,
+                   int64_t* n_out, void* stream) {
+  using namespace mc;
+  if (!spec_ok(s)) return MC_EINVAL;
+  if (!data || !payload || !n_out) { set_error("null pointer"); return MC_EINVAL; }
+  if (len < 22) { set_error("payload shorter than header"); return MC_EINVAL; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t raw[22];
+  if (cudaMemcpyAsync(raw, data, 22, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("reading payload header failed");
+    return MC_ECUDA;
+  }
+  // "<BBQIII" (compressors.py:53, 623-645)
+  uint64_t n;
+  uint32_t nidx, nval, nbits;
+  memcpy(&n, raw + 2, 8);
+  memcpy(&nidx, raw + 10, 4);
+  memcpy(&nval, raw + 14, 4);
+  memcpy(&nbits, raw + 18, 4);
+  const int algo = raw[0];
+  if (algo >= MC_NUM_ALGORITHMS) { set_error("unknown algorithm id %d", algo); return MC_EINVAL; }
+  const int64_t expect = 22 + 4 * (int64_t)nidx + 4 * (int64_t)nval + (int64_t)nbits;
+  if (len != expect) { set_error("payload length %lld does not match header (%lld)", (long long)len, (long long)expect); return MC_EINVAL; }
+  if (algo != s->algorithm) { set_error("payload algorithm id %d does not match spec id %d", algo, s->algorithm); return MC_EINVAL; }
+  if (n < 1) { set_error("corrupt payload: zero length"); return MC_EINVAL; }
+  const bool sparse = is_sparse(algo);
+  mc_layout L;
+  if (fill_layout(s, (int64_t)n, sparse ? (int64_t)(nidx > 0 ? nidx : 1) : 0, &L) != MC_OK) return MC_EINVAL;
+  DeserArgs a{};
+  uint8_t* p = static_cast<uint8_t*>(payload);
+  if (sparse) {
+    if (nidx != nval) { set_error("corrupt payload: index/value length mismatch"); return MC_EINVAL; }
+    if (nbits != 0) { set_error("corrupt payload: sparsifier payload carries bits"); return MC_EINVAL; }
+    if (algo != MC_THRESHOLD && (int64_t)nidx != L.cap) { set_error("corrupt payload: expected %lld indices", (long long)L.cap); return MC_EINVAL; }
+    L.cap = nidx;
+    L.n_val = nidx;
+    L.off_val = HDR + a16(4 * (int64_t)nidx);
+    L.bytes = L.off_val + a16(4 * (int64_t)nidx);
+    a.dst[0] = p + HDR;
+    a.dst[1] = p + L.off_val;
+  } else {
+    if (nidx != 0) { set_error("corrupt payload: dense payload carries indices"); return MC_EINVAL; }
+    if ((int64_t)nval != L.n_val) { set_error("corrupt payload: value count %u, expected %lld", nval, (long long)L.n_val); return MC_EINVAL; }
+    if ((int64_t)nbits != L.n_bits + L.n_codes) { set_error("corrupt payload: bit buffer length %u, expected %lld", nbits, (long long)(L.n_bits + L.n_codes)); return MC_EINVAL; }
+    a.dst[0] = p + HDR;
+    a.dst[1] = p + L.off_val;
+    a.dst[2] = p + L.off_bits;
+    a.dst[3] = p + L.off_codes;
+  }
+  if (payload_cap < L.bytes) { set_error("payload buffer too small (%lld < %lld)", (long long)payload_cap, (long long)L.bytes); return MC_EINVAL; }
+  a.len[0] = 4 * (int64_t)nidx;
+  a.len[1] = 4 * (int64_t)nval;
+  a.len[2] = sparse ? 0 : L.n_bits;
+  a.len[3] = sparse ? 0 : L.n_codes;
+  a.start[0] = 22;
+  for (int i = 0; i < 4; ++i) a.start[i + 1] = a.start[i] + a.len[i];
+  a.h.algorithm = (uint32_t)algo;
+  a.h.flags = raw[1];
+  a.h.original_len = n;
+  a.h.n_idx = nidx;
+  a.h.n_val = nval;
+  a.h.n_bits = nbits;
+  a.h.cap = sparse ? nidx : 0;
+  a.in = static_cast<const uint8_t*>(data);
+  a.payload = p;
+  *n_out = (int64_t)n;
+  const unsigned grid = (unsigned)imax(1, imin(cdiv(len, 256), 4096));
+  note_launch(); k_deserialize<<<grid, 256, 0, st>>>(a);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }

@@ -104,7 +104,9 @@ class GradSync:
         key = partition.boundaries
         plan = self._plans.get(key)
         if plan is not None:
+            self._plans[key] = self._plans.pop(key)  # most recently used last
             return plan
+        self._evict()
         plan = []
         ef = self.spec.uses_error_feedback
         mom = self.spec.momentum_coef is not None
@@ -123,12 +125,39 @@ class GradSync:
         self._plans[key] = plan
         return plan
 
+    # candidate partitions a measured search keeps alive besides the pinned one; each holds
+    # an fp64 residual (8 B/elem) plus payload / gather buffers, so a Y>=3 search over
+    # hundreds of candidates must not keep them all (the reference keeps every state on the
+    # host, trainer.py:380; an evicted candidate restarts from zero state if revisited)
+    MAX_CACHED_PLANS = 4
+
+    def _evict(self) -> None:
+        keep = {self.partition.boundaries} if hasattr(self, "partition") else set()
+        graph = getattr(self, "_graph", None)
+        if graph is not None:
+            keep.add(graph[0])
+        while len(self._plans) >= self.MAX_CACHED_PLANS + len(keep):
+            victim = next((k for k in self._plans if k not in keep), None)
+            if victim is None:
+                break
+            self._drop(victim)
+
+    def _drop(self, key) -> None:
+        self._plans.pop(key, None)
+        graph = getattr(self, "_graph", None)
+        if graph is not None and graph[0] == key:
+            self._graph = None  # the graph holds raw pointers into the dropped buffers
+        peer = getattr(self, "_peer", None)
+        if peer is not None:
+            for k in [k for k in peer["groups"] if k[0] == key]:
+                del peer["groups"][k]
+
     def drop_state(self, partition: Optional[Partition] = None) -> None:
-        """Free the EF/momentum state and buffers of one (or every) partition."""
-        if partition is None:
-            self._plans.clear()
-        else:
-            self._plans.pop(partition.boundaries, None)
+        """Free the EF/momentum state and buffers of one (or every) partition, together with
+        a CUDA Graph captured over them and their peer-exchange buffers."""
+        keys = list(self._plans) if partition is None else [partition.boundaries]
+        for k in keys:
+            self._drop(k)
 
     def set_gradients(self, flat: torch.Tensor) -> None:
         self.flat.copy_(flat, non_blocking=True)
@@ -185,7 +214,7 @@ class GradSync:
         self.partition = part
         plan = self._plan(part)
         need = max(_native.workspace_bytes(self.cspec, grp.n) for grp in plan)
-        ws = _WS.get(self.device, need)  # sized before capture: the graph keeps these pointers
+        ws = _WS.get(self.device, need, self.stream)  # sized before capture: the graph keeps these pointers
         graph = torch.cuda.CUDAGraph()
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.graph(graph, stream=self.stream):
@@ -412,7 +441,7 @@ class GradSync:
         sh, se, sd = _stream_ptr(self._h2d), _stream_ptr(self.stream), _stream_ptr(self._d2h)
         for g, grp in enumerate(plan):
             lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
-            ws = _WS.get(self.device, _native.workspace_bytes(self.cspec, grp.n))
+            ws = _WS.get(self.device, _native.workspace_bytes(self.cspec, grp.n), self.stream)
             _native.check(lib.mc_pipe_group(
                 self._pipe, ctypes.byref(self.cspec), host_in.data_ptr() + 4 * grp.start,
                 host_out.data_ptr() + 4 * grp.start, self.flat.data_ptr() + 4 * grp.start, grp.n, chunk_elems,
@@ -501,12 +530,26 @@ class GradSync:
         self._hooks = []
 
     def check(self) -> None:
-        """Raise the reference's ValueError if any device error flag was set."""
+        """Raise the reference's ValueError if any device error flag was set.
+
+        Non-finite gradients: the reference raises before touching codec state
+        (compressors.py:384-385); the engine's kernels consume a group in one in-place pass,
+        so the steps since the last check() may have folded the non-finite values into the
+        EF residual / momentum.  Rather than carry NaN forever, the state of every cached
+        partition is reset to zeros (the codec memory at t = 0) before raising — a skipped
+        (e.g. AMP overflow) step costs the EF memory, not the run."""
         flags = int(self.err.item())
         if flags:
             self.err.zero_()
             from .compressors import _raise_flags
 
+            if flags & _native.MC_ERR_NONFINITE:
+                for plan in self._plans.values():
+                    for grp in plan:
+                        if grp.residual is not None:
+                            grp.residual.zero_()
+                        if grp.momentum is not None:
+                            grp.momentum.zero_()
             _raise_flags(flags)
 
     # ------------------------------------------------------------ scheduler handle

@@ -203,3 +203,35 @@ def test_quantizer_scale_range_matches_oracle(algo, ef, C):
         if ef:
             _eq_bits(st_d.residual.cpu().numpy(), np.asarray(st_r.residual), f"{algo} t{t} residual")
         _eq_bits(C.aggregate(spec, [p_dev]).cpu().numpy(), np.asarray(O.aggregate(spec, [p_ref])), f"{algo} t{t} mean")
+
+
+@pytest.mark.parametrize("algo", ["identity", "fp16", "topk", "randk", "dgc_lite", "threshold", "qsgd", "signsgd",
+                                  "efsignsgd", "onebit", "signum", "terngrad", "int8"])
+def test_serialize_deserialize_roundtrip_on_device(algo, C):
+    """Acceptance #8(d) (test_acceptance.py:283-291) through the device ABI: the canonical
+    bytes from mc_serialize, parsed back by mc_deserialize (and by the host deserialize),
+    decode to the same gradient and re-serialize to the same bytes."""
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    spec = CompressorSpec(algo, error_feedback=False)
+    rng = np.random.default_rng(8)
+    for n in (1, 63, 513, 2048, 100_003):
+        x = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).cuda()
+        p, _ = C.encode(spec, x, seed=3)
+        raw = C.serialize(p)
+        assert len(raw) == p.byte_size
+        back_d = C.device_deserialize(spec, raw)
+        back_h = C.deserialize(raw)
+        assert back_d.on_device and not back_h.on_device
+        ref = C.decode(spec, p).cpu().numpy()
+        assert np.array_equal(C.decode(spec, back_d).cpu().numpy().view(np.uint32), ref.view(np.uint32)), (algo, n)
+        assert np.array_equal(np.asarray(C.decode(spec, back_h)).view(np.uint32), ref.view(np.uint32)), (algo, n)
+        assert C.serialize(back_d) == raw, (algo, n)
+        assert C.serialize(back_h) == raw, (algo, n)
+    # malformed input: the reference's errors (compressors.py:623-645)
+    with pytest.raises(ValueError, match="shorter than header"):
+        C.device_deserialize(spec, raw[:10])
+    with pytest.raises(ValueError, match="does not match header"):
+        C.device_deserialize(spec, raw + b"\0")
+    with pytest.raises(ValueError, match="unknown algorithm id"):
+        C.device_deserialize(spec, bytes([99]) + raw[1:])

@@ -245,3 +245,59 @@ def test_graph_capture_rejects_stochastic_codecs():
     s = GradSync(CompressorSpec("qsgd"), gradsets.profile("resnet50_161"))
     with pytest.raises(ValueError):
         s.capture_graph()
+
+
+def test_drop_state_releases_captured_graph_and_caps_cached_plans():
+    """a CUDA Graph captured over a partition's buffers must die with them, and a
+    measured search must not keep every candidate's fp64 residual alive."""
+    from paper_2103_15195_b200 import gradsets
+    from paper_2103_15195_b200.profiles import Partition
+    from paper_2103_15195_b200.spec import CompressorSpec
+    from paper_2103_15195_b200.sync import GradSync
+
+    prof = gradsets.profile("tiny40")
+    sync = GradSync(CompressorSpec("efsignsgd"), prof, partition=Partition(prof.n_tensors, (7,)))
+    sync.capture_graph()
+    assert sync._graph is not None
+    sync.drop_state(Partition(prof.n_tensors, (7,)))
+    assert sync._graph is None and not sync._plans
+    sync.step()  # eager again, fresh zero state
+    for cut in range(1, 20):  # a search visiting 19 candidates
+        sync.timed_iteration(Partition(prof.n_tensors, (cut,)))
+    assert len(sync._plans) <= GradSync.MAX_CACHED_PLANS + 1
+    assert sync.partition.boundaries in sync._plans
+
+
+def test_nonfinite_gradient_leaves_no_nan_state():
+    """encode() never mutates the caller's device state (the reference raises
+    before touching it), and the engine resets the poisoned EF state when check() raises."""
+    from paper_2103_15195_b200 import compressors as C
+    from paper_2103_15195_b200 import gradsets
+    from paper_2103_15195_b200.spec import CompressorSpec
+    from paper_2103_15195_b200.sync import GradSync
+
+    spec = CompressorSpec("efsignsgd")
+    x = torch.randn(10_000, device="cuda")
+    _, st = C.encode(spec, x, None)
+    before = st.residual.clone()
+    bad = x.clone()
+    bad[17] = float("nan")
+    with pytest.raises(ValueError, match="non-finite"):
+        C.encode(spec, bad, st)
+    assert torch.equal(st.residual.view(torch.int64), before.view(torch.int64))
+    _, st2 = C.encode(spec, x, st)
+    assert st2.residual is not st.residual  # a new state object, as in the reference
+
+    prof = gradsets.profile("tiny40")
+    sync = GradSync(spec, prof)
+    sync.flat.copy_(torch.from_numpy(gradsets.synthetic_gradients("tiny40", 0, 0)))
+    sync.flat[5] = float("inf")
+    sync.step()
+    with pytest.raises(ValueError, match="non-finite"):
+        sync.check()
+    res = sync._plan(sync.partition)[0].residual
+    assert bool(torch.isfinite(res).all()) and not bool(res.any())
+    sync.flat.copy_(torch.from_numpy(gradsets.synthetic_gradients("tiny40", 1, 0)))
+    sync.step()
+    sync.check()
+    assert bool(torch.isfinite(sync.flat).all())

@@ -193,3 +193,14 @@ def test_exhaustive_matches_heuristic_on_unimodal():
     he = heuristic_search(SearchConfig(Y=2, evaluator=f), prof)
     assert ex.partition == he.partition == Partition(12, (4,))
     assert naive_partition(prof, 5).group_counts() == [3, 3, 2, 2, 2]
+
+
+def test_package_root_reexports_reference_names():
+    """mergesched/__init__.py:20-43 re-exports, minus the out-of-scope trainer types."""
+    import paper_2103_15195_b200 as P
+
+    for name in ("LayerProfile", "ModelProfile", "Partition", "CompressorSpec", "CompressedPayload",
+                 "ResidualState", "CostParams", "TimingSample", "SimConfig", "SimReport", "SearchConfig",
+                 "SearchResult"):
+        assert getattr(P, name).__name__ == name
+        assert name in P.__all__
