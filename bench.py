@@ -43,12 +43,13 @@ def parse():
     ap.add_argument("--search-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="elements per pipelined H2D/encode/D2H chunk")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl", "allreduce_dense"],
                     help="N > 1: fused encode + push over NVLink peer memory (falls back to NCCL if the "
                          "peer mapping fails on any rank), the NCCL allgather, or auto: the push where the "
                          "payload is >= 1/8 of the fp32 gradient (byte codecs, where overlapping the exchange "
                          "with the encode pays; profiles/r1_projection_multi_gpu.jsonl), NCCL for the 1-bit "
-                         "and sparse codecs")
+                         "and sparse codecs; allreduce_dense: the uncompressed fp32 NCCL all_reduce + /N "
+                         "baseline of BASELINE config 5 (codec ignored)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU oracle sample budget")
     ap.add_argument("--json-out", default=None)
@@ -120,6 +121,77 @@ class ClockSampler:
         names = [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"]
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
                 "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ host placement + PCIe probe (e2e context)
+def numa_bind(device_index: int):
+    """Pin this process to the CPUs of the GPU's NUMA node (read from sysfs) before the
+    pinned host buffers are allocated and first touched, so the e2e copies do not cross the
+    socket interconnect.  Returns {"node", "cpus"} or None where sysfs has no answer."""
+    try:
+        import torch
+
+        pr = torch.cuda.get_device_properties(device_index)
+        bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        node = int(Path(f"/sys/bus/pci/devices/{bdf}/numa_node").read_text().strip())
+        if node < 0:
+            return {"node": node, "cpus": None, "bdf": bdf}
+        cpus = set()
+        for part in Path(f"/sys/devices/system/node/node{node}/cpulist").read_text().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return {"node": node, "cpus": len(cpus), "bdf": bdf}
+    except Exception:  # noqa: BLE001 - placement is best effort, reported as unknown
+        return None
+
+
+def pcie_probe(host_in, host_out, dev, reps: int = 10):
+    """Same-run bound of the e2e leg: the step's H2D of ``host_in`` and D2H into ``host_out``
+    (pinned, the e2e's own buffers) issued together on two streams — PCIe full duplex.
+    Returns GB/s of fp32 gradient (bytes of one direction / time), CUDA events."""
+    import torch
+
+    n = host_in.numel()
+    da = torch.empty(n, dtype=torch.float32, device=dev)
+    db = torch.zeros(n, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    cur = torch.cuda.current_stream(dev)
+
+    def one():
+        for st in (s1, s2):
+            st.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            da.copy_(host_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            host_out.copy_(db, non_blocking=True)
+        for st in (s1, s2):
+            cur.wait_stream(st)
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        for _ in range(reps):
+            fn()
+        b.record(cur)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b) / reps
+
+    def h2d():
+        da.copy_(host_in, non_blocking=True)
+
+    def d2h():
+        host_out.copy_(db, non_blocking=True)
+
+    B = 4.0 * n
+    r = {"duplex_GBps": B / timed(one) / 1e6, "h2d_GBps": B / timed(h2d) / 1e6, "d2h_GBps": B / timed(d2h) / 1e6}
+    del da, db
+    return r
 
 
 # ------------------------------------------------------------------ CPU oracle timing
@@ -269,6 +341,7 @@ def main():
     local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    placement = numa_bind(local)
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -278,9 +351,18 @@ def main():
     prof = gradsets.profile(args.gradset)
     D = prof.total_size
 
+    dense = args.exchange == "allreduce_dense"
+    if dense:
+        from paper_2103_15195_b200.spec import CompressorSpec
+
+        spec = CompressorSpec("identity")
+        args.no_search = args.no_search or not args.boundaries
     sync = GradSync(spec, prof, root_seed=0, device=dev)
     exchange_used = "none (one rank)"
-    if world > 1:
+    if dense:
+        sync.use_dense_allreduce()
+        exchange_used = "uncompressed fp32 NCCL all_reduce(SUM) + /N per group (config 5 comparator)"
+    elif world > 1:
         exchange_used = "nccl allgather"
         from paper_2103_15195_b200.spec import payload_bytes
 
@@ -380,6 +462,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = world * 4.0 * D / (e2e_ms / args.e2e_steps * 1e-3) / 1e9
+    pcie = pcie_probe(host_grads, out_host, dev)  # same buffers, same run: what bounds e2e here
 
     # ---- CPU baseline: the oracle on this host, rank 0 at N=1 only, bounded sample
     cpu = None
@@ -432,7 +515,9 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * D, "d2h_bytes_per_step": 4 * D,
-                    "ms_per_step": e2e_ms / args.e2e_steps},
+                    "ms_per_step": e2e_ms / args.e2e_steps,
+                    "pcie": pcie, "pcie_frac": e2e_value / world / pcie["duplex_GBps"],
+                    "host_placement": placement},
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
         }

@@ -6,8 +6,12 @@
  * extern "C", takes plain pointers and sizes (device pointers unless stated),
  * returns an int status (MC_OK = 0, negative on argument/CUDA errors) and never
  * throws.  All device work is stream-ordered on the caller's cudaStream_t
- * (passed as void*); the library keeps no global mutable state except a cached
- * SM count.  Data-dependent errors (non-finite gradients, corrupt indices) are
+ * (passed as void*).  The library never allocates device memory (callers pass workspaces:
+ * mc_encode_workspace_bytes / mc_decode_workspace_bytes) and keeps only process-wide caches
+ * that do not change results: the SM count per device, per-(kernel, device) "dynamic shared
+ * memory opted in" bits, a launch counter (statistics), environment tuning knobs read once,
+ * and a mutex-guarded host table of randk rejection-drift statistics per (n, k) shape that
+ * only sizes the speculative walk.  Data-dependent errors (non-finite gradients, corrupt indices) are
  * OR-ed into a caller-owned device word `err_flags` and surface at the
  * caller's next sync point, where the Python layer raises the reference's
  * ValueError.
@@ -39,6 +43,7 @@ extern "C" {
 #define MC_EINVAL (-1)       /* bad argument (null pointer, n < 1, bad spec) */
 #define MC_ECUDA (-2)        /* a CUDA launch or runtime call failed */
 #define MC_EWORKSPACE (-3)   /* workspace smaller than mc_encode_workspace_bytes() */
+#define MC_EPEER (-4)        /* the devices cannot reach each other over P2P (NVLink / PCIe) */
 
 /* device error flags, OR-ed into *err_flags */
 #define MC_ERR_NONFINITE 0x1u    /* "gradient contains non-finite values"   compressors.py:384-385 */
@@ -136,6 +141,13 @@ int mc_encode_range(const mc_spec* spec, const float* grad, int64_t n, int64_t b
  * order in fp32 exactly as aggregate().  Payload r lives at payloads + r*stride_bytes. */
 int mc_decode_mean(const mc_spec* spec, const void* payloads, int64_t stride_bytes, int32_t nranks,
                    int64_t n, float* out, uint32_t* err_flags, void* stream);
+/* The same with caller-owned scratch: the sparsifiers' decode keeps a per-(rank, output tile)
+ * start table of mc_decode_workspace_bytes(spec, n, nranks) bytes (0 for the dense codecs);
+ * mc_decode_mean passes none and returns MC_EWORKSPACE for them.  The library never
+ * allocates device memory. */
+int64_t mc_decode_workspace_bytes(const mc_spec* spec, int64_t n, int32_t nranks);
+int mc_decode_mean_ws(const mc_spec* spec, const void* payloads, int64_t stride_bytes, int32_t nranks, int64_t n,
+                      float* out, void* workspace, int64_t workspace_bytes, uint32_t* err_flags, void* stream);
 
 /* Merge stage: gather `count` device tensors (host array of device pointers)
  * into one contiguous buffer in list order / scatter it back. */
@@ -162,7 +174,9 @@ int mc_deserialize(const mc_spec* spec, const void* data, int64_t len, void* pay
  * mapped pointers, the entry equal to `payload` is the local one); when all of it is
  * system-visible, *flags[j] := epoch for every j (rank j's flag word for this rank).  The
  * pipe-kernel codecs (efsignsgd, onebit, int8) store into the peer slots from the encode
- * kernel itself; the others encode, then copy.  mc_push_wait: the stream waits until the
+ * kernel itself; the others encode, then copy — threshold (data-dependent count in a
+ * capacity-n slot) copies only the header and the first n_idx entries, read on the device, so
+ * the variable-size exchange needs no host round trip.  mc_push_wait: the stream waits until the
  * local flags[0..nranks) all equal epoch — the gathered payloads are then complete in rank
  * order, exactly what mc_decode_mean reads (replaces the NCCL allgather of trainer.py:377-389).
  * A peer silent for timeout_ns (0 = MC_PUSH_TIMEOUT_DEFAULT_NS) sets MC_ERR_PEER_TIMEOUT and
@@ -173,6 +187,15 @@ int mc_encode_push(const mc_spec* spec, const float* grad, int64_t n, double* re
                    void* stream);
 int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,
                  void* stream);
+
+/* Peer exchange set-up (replaces nothing in the reference: its "allgather" is a Python list,
+ * trainer.py:377-389).  mc_peer_enable: let kernels on `device` load/store memory of
+ * `peer_device` (cudaDeviceEnablePeerAccess; a no-op when equal, MC_EPEER when the pair has
+ * no P2P path).  mc_peer_probe: one kernel on the calling stream's device stores `value` to
+ * every dsts[j] (peer-mapped pointers) at system scope — the store-then-readback probe that
+ * proves a mapping before any encode kernel pushes through it. */
+int mc_peer_enable(int32_t device, int32_t peer_device);
+int mc_peer_probe(uint32_t* const* dsts, int32_t n, uint32_t value, void* stream);
 
 /* Host-buffer sync of one rank (world size 1), enqueued natively: the trainer's step on a
  * worker's host gradient (trainer.py:360-395, one worker).  For each group: H2D of

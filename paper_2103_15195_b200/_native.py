@@ -17,6 +17,7 @@ from .spec import McSpec
 LIB_PATH = Path(__file__).resolve().parent / "libmergecomp.so"
 
 MC_OK = 0
+MC_EPEER = -4
 MC_ERR_NONFINITE = 0x1
 MC_ERR_INDEX_RANGE = 0x2
 MC_ERR_INDEX_ORDER = 0x4
@@ -61,6 +62,9 @@ _SIGS = {
     "mc_encode_range": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P,
                                        ctypes.c_uint64, ctypes.c_uint64, _P, _P, ctypes.c_int64, _P, _P, _P]),
     "mc_decode_mean": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, _P, _P, _P]),
+    "mc_decode_workspace_bytes": (ctypes.c_int64, [_SPEC, ctypes.c_int64, ctypes.c_int32]),
+    "mc_decode_mean_ws": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, _P, _P,
+                                         ctypes.c_int64, _P, _P]),
     "mc_pack": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P, _P]),
     "mc_unpack": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, _P]),
     "mc_serialize": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), _P]),
@@ -70,6 +74,8 @@ _SIGS = {
                                       ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_uint32, _P,
                                       ctypes.c_int64, _P, _P]),
     "mc_push_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, _P, _P]),
+    "mc_peer_enable": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32]),
+    "mc_peer_probe": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_uint32, _P]),
     "mc_pipe_create": (ctypes.c_int, [ctypes.POINTER(_P)]),
     "mc_pipe_destroy": (None, [_P]),
     "mc_pipe_group": (ctypes.c_int, [_P, _SPEC, _P, _P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, ctypes.c_uint64,

@@ -301,10 +301,16 @@ def push_wait(flags: torch.Tensor, nranks: int, epoch: int, err: Optional[torch.
 def device_decode_mean(spec: CompressorSpec, base: torch.Tensor, stride: int, nranks: int, n: int,
                        out: torch.Tensor, err: torch.Tensor, stream=None, cspec=None) -> None:
     cs = cspec if cspec is not None else spec.to_c()
+    lib = _native.lib()
+    need = int(lib.mc_decode_workspace_bytes(ctypes.byref(cs), n, nranks))
+    if need < 0:
+        _native.check(need, "mc_decode_workspace_bytes")
+    ws = _WS.get(out.device, need, stream) if need > 0 else None  # stream-ordered after the encodes
     _native.check(
-        _native.lib().mc_decode_mean(ctypes.byref(cs), base.data_ptr(), stride, nranks, n, out.data_ptr(),
-                                     err.data_ptr(), _stream_ptr(stream)),
-        "mc_decode_mean",
+        lib.mc_decode_mean_ws(ctypes.byref(cs), base.data_ptr(), stride, nranks, n, out.data_ptr(),
+                              None if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                              err.data_ptr(), _stream_ptr(stream)),
+        "mc_decode_mean_ws",
     )
 
 

@@ -24,14 +24,16 @@ void set_error(const char* fmt, ...) {
 }
 
 int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cached[64];  // per device (zero = not read yet)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& c = cached[dev & 63];
+  int v = c.load(std::memory_order_relaxed);
+  if (!v) {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
-    cached = v;
+    c.store(v, std::memory_order_relaxed);
   }
-  return cached;
+  return v;
 }
 
 // max(1, ceil(round((1 - s) * n, 9)))  — compressors.py:185-194.  Python's round(x, 9)
@@ -150,7 +152,10 @@ int64_t mc_encode_workspace_bytes(const mc_spec* s, int64_t n) {
     case MC_IDENTITY: case MC_FP16: return 64;
     case MC_QSGD: case MC_EFSIGNSGD: case MC_ONEBIT: case MC_TERNGRAD: case MC_INT8: return bucket_ws_bytes(s, n);
     case MC_SIGNSGD: case MC_SIGNUM: return signglobal_ws_bytes(s, n);
-    default: return sparse_ws_bytes(s, n);
+    default: {  // the fused single-rank path decodes its own sparse payload in this scratch
+      const int64_t e = sparse_ws_bytes(s, n), d = decode_sparse_ws_bytes(n, 1);
+      return e > d ? e : d;
+    }
   }
 }
 
@@ -272,15 +277,32 @@ struct PushArgs {
   uint32_t* flag[MC_MAX_PUSH];
   uint32_t epoch;
   uint32_t* done;
+  int64_t off_idx, off_val;  // sparse (threshold): only the header and the first n_idx entries move
+  int sparse;
 };
 // Copy a finished payload into every peer slot (16-byte vectors, all CTAs), then the last
-// CTA releases every rank's flag for this rank at system scope.
+// CTA releases every rank's flag for this rank at system scope.  Threshold payloads have a
+// data-dependent count inside a capacity-n buffer: the kernel reads n_idx from the device
+// header and moves the header plus idx[0, n_idx) and val[0, n_idx) only — the variable-size
+// exchange needs no host round trip (counts, then a padded gather).
 __global__ void __launch_bounds__(256) k_push_copy(PushArgs a) {
-  const int64_t nv = a.bytes / 16;
   const uint4* src = reinterpret_cast<const uint4*>(a.src);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 v = src[i];
-    for (int j = 0; j < a.ndst; ++j) reinterpret_cast<uint4*>(a.dst[j])[i] = v;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  if (!a.sparse) {
+    const int64_t nv = a.bytes / 16;
+    for (int64_t i = tid; i < nv; i += nth) {
+      const uint4 v = src[i];
+      for (int j = 0; j < a.ndst; ++j) reinterpret_cast<uint4*>(a.dst[j])[i] = v;
+    }
+  } else {
+    const int64_t cnt = reinterpret_cast<const mc_payload_header*>(a.src)->n_idx;
+    const int64_t nsec = (4 * cnt + 15) / 16;  // 16-byte vectors per section
+    const int64_t hv = sizeof(mc_payload_header) / 16, iv = a.off_idx / 16, vv = a.off_val / 16;
+    for (int64_t t = tid; t < hv + 2 * nsec; t += nth) {
+      const int64_t i = t < hv ? t : (t < hv + nsec ? iv + (t - hv) : vv + (t - hv - nsec));
+      const uint4 v = src[i];
+      for (int j = 0; j < a.ndst; ++j) reinterpret_cast<uint4*>(a.dst[j])[i] = v;
+    }
   }
   __threadfence_system();  // this thread's peer stores, system-wide, before the CTA counts in
   if (last_cta(a.done)) {
@@ -313,10 +335,28 @@ __global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch, uint64
 }
 }  // namespace
 
-int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a, cudaStream_t st) {
+// One store per destination from THIS device (the kernel runs where the encode kernels
+// will), then a system-scope fence: the peer-exchange probe of GradSync.try_peer_exchange.
+struct ProbeArgs {
+  uint32_t* dst[MC_MAX_PUSH];
+  int n;
+  uint32_t value;
+};
+__global__ void k_peer_probe(ProbeArgs a) {
+  for (int j = threadIdx.x; j < a.n; j += blockDim.x) st_release_sys(a.dst[j], a.value);
+  __threadfence_system();
+}
+
+int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a, cudaStream_t st,
+                     const mc_layout* sparse) {
   PushArgs pa{};
   pa.src = payload;
   pa.bytes = (bytes + 15) / 16 * 16;
+  if (sparse) {
+    pa.sparse = 1;
+    pa.off_idx = sparse->off_idx;
+    pa.off_val = sparse->off_val;
+  }
   for (int j = 0; j < a.npush; ++j) {
     pa.flag[pa.nflag++] = a.push_flags[j];
     if (a.push_dsts[j] != (void*)payload) pa.dst[pa.ndst++] = static_cast<uint8_t*>(a.push_dsts[j]);
@@ -354,7 +394,8 @@ int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* resid
   a.push_dsts = dsts;
   a.push_flags = flags;
   a.epoch = epoch;
-  return launch_push_copy(static_cast<const uint8_t*>(payload), L.bytes, a, static_cast<cudaStream_t>(stream));
+  return launch_push_copy(static_cast<const uint8_t*>(payload), L.bytes, a, static_cast<cudaStream_t>(stream),
+                          s->algorithm == MC_THRESHOLD ? &L : nullptr);
 }
 
 int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,
@@ -363,6 +404,43 @@ int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t
   if (timeout_ns == 0) timeout_ns = MC_PUSH_TIMEOUT_DEFAULT_NS;
   note_launch();
   k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, epoch, timeout_ns, err_flags);
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+
+int mc_peer_enable(int32_t device, int32_t peer_device) {
+  if (device < 0 || peer_device < 0) { set_error("bad device index"); return MC_EINVAL; }
+  if (device == peer_device) return MC_OK;  // ranks sharing one GPU: plain device memory
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, device, peer_device) != cudaSuccess || !can) {
+    cudaGetLastError();
+    set_error("device %d cannot access device %d over P2P", device, peer_device);
+    return MC_EPEER;
+  }
+  int prev = 0;
+  MC_API_CHECK(cudaGetDevice(&prev));
+  MC_API_CHECK(cudaSetDevice(device));
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  cudaSetDevice(prev);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); return MC_OK; }
+  if (e != cudaSuccess) {
+    set_error("cudaDeviceEnablePeerAccess(%d -> %d): %s", device, peer_device, cudaGetErrorString(e));
+    return MC_EPEER;
+  }
+  return MC_OK;
+}
+
+int mc_peer_probe(uint32_t* const* dsts, int32_t n, uint32_t value, void* stream) {
+  if (!dsts || n < 1 || n > MC_MAX_PUSH) { set_error("bad probe destinations"); return MC_EINVAL; }
+  mc::ProbeArgs a{};
+  a.n = n;
+  a.value = value;
+  for (int j = 0; j < n; ++j) {
+    if (!dsts[j]) { set_error("null probe destination"); return MC_EINVAL; }
+    a.dst[j] = dsts[j];
+  }
+  mc::note_launch();
+  mc::k_peer_probe<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
@@ -383,11 +461,17 @@ int mc_encode_decode(const mc_spec* s, const float* grad, int64_t n, double* res
   const int rc = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
                              err_flags, stream, out);
   if (rc != MC_FUSED_UNSUPPORTED) return rc;
-  return mc_decode_mean(s, payload, 0, 1, n, out, err_flags, stream);  // two-pass codecs: decode own payload
+  // two-pass codecs: decode the own payload; the encode's scratch is free again in stream order
+  return mc_decode_mean_ws(s, payload, 0, 1, n, out, workspace, workspace_bytes, err_flags, stream);
 }
 
-int mc_decode_mean(const mc_spec* s, const void* payloads, int64_t stride_bytes, int32_t nranks, int64_t n, float* out,
-                   uint32_t* err_flags, void* stream) {
+int64_t mc_decode_workspace_bytes(const mc_spec* s, int64_t n, int32_t nranks) {
+  if (!spec_ok(s) || n < 1 || nranks < 1) return MC_EINVAL;
+  return is_sparse(s->algorithm) ? decode_sparse_ws_bytes(n, nranks) : 0;
+}
+
+int mc_decode_mean_ws(const mc_spec* s, const void* payloads, int64_t stride_bytes, int32_t nranks, int64_t n,
+                      float* out, void* workspace, int64_t workspace_bytes, uint32_t* err_flags, void* stream) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1 || nranks < 1 || !payloads || !out || !err_flags) { set_error("bad decode arguments"); return MC_EINVAL; }
   if (nranks > 1 && stride_bytes < 32) { set_error("stride too small"); return MC_EINVAL; }
@@ -395,8 +479,13 @@ int mc_decode_mean(const mc_spec* s, const void* payloads, int64_t stride_bytes,
   if (fill_layout(s, n, 0, &L) != MC_OK) return MC_EINVAL;
   Ctx c{static_cast<cudaStream_t>(stream), err_flags};
   const uint8_t* base = static_cast<const uint8_t*>(payloads);
-  if (is_sparse(s->algorithm)) return decode_mean_sparse(s, L, base, stride_bytes, nranks, out, c);
+  if (is_sparse(s->algorithm)) return decode_mean_sparse(s, L, base, stride_bytes, nranks, out, c, workspace, workspace_bytes);
   return decode_mean_dense(s, L, base, stride_bytes, nranks, out, c);
+}
+
+int mc_decode_mean(const mc_spec* s, const void* payloads, int64_t stride_bytes, int32_t nranks, int64_t n, float* out,
+                   uint32_t* err_flags, void* stream) {
+  return mc_decode_mean_ws(s, payloads, stride_bytes, nranks, n, out, nullptr, 0, err_flags, stream);
 }
 
 }  // extern "C"
@@ -405,54 +494,77 @@ int mc_decode_mean(const mc_spec* s, const void* payloads, int64_t stride_bytes,
 namespace mc {
 namespace {
 
-constexpr int PACK_MAX = 128;
+// Merge stage (K1 / K11 of SURVEY.md §2.1): per-layer gradients <-> one fused buffer in list
+// order.  Work is split on the host into CTA chunks of PACK_CHUNK elements of ONE tensor
+// (blk0[i] = first chunk of tensor i), so a CTA finds its tensor with one uniform binary
+// search over the parameter table and then streams a contiguous run: 128-bit loads and
+// stores whenever source and destination share their 16-byte phase (a scalar head aligns
+// them), scalar otherwise.  Pure HBM copy: 8 B/element.
+constexpr int PACK_MAX = 512;    // tensors per launch (parameter table, ~14 KB)
+constexpr int PACK_CHUNK = 8192;  // elements per CTA
 struct PackArgs {
   const float* src[PACK_MAX];
   float* dst[PACK_MAX];
   int64_t off[PACK_MAX + 1];  // element offset of tensor i inside the fused buffer
+  int32_t blk0[PACK_MAX + 1];  // first CTA chunk of tensor i
   int count;
   int to_fused;  // 1: pack (tensors -> fused), 0: unpack (fused -> tensors)
   float* fused;
   const float* cfused;
 };
 
-__global__ void k_pack(PackArgs a) {
-  const int64_t total = a.off[a.count];
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = a.count - 1;  // tensor holding element e: largest i with off[i] <= e
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (a.off[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    const int64_t j = e - a.off[lo];
-    if (a.to_fused) a.fused[e] = a.src[lo][j];
-    else a.dst[lo][j] = a.cfused[e];
+__global__ void __launch_bounds__(256) k_pack(const __grid_constant__ PackArgs a) {
+  const int b = blockIdx.x;
+  int lo = 0, hi = a.count - 1;  // tensor of this chunk: largest i with blk0[i] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.blk0[mid] <= b) lo = mid; else hi = mid - 1;
   }
+  const int64_t numel = a.off[lo + 1] - a.off[lo];
+  const int64_t j0 = (int64_t)(b - a.blk0[lo]) * PACK_CHUNK;
+  const int64_t len = imin(PACK_CHUNK, numel - j0);
+  const float* src = a.to_fused ? a.src[lo] + j0 : a.cfused + a.off[lo] + j0;
+  float* dst = a.to_fused ? a.fused + a.off[lo] + j0 : a.dst[lo] + j0;
+  const uintptr_t ps = (uintptr_t)src & 15, pd = (uintptr_t)dst & 15;
+  int64_t head = 0;
+  if (ps == pd) head = imin(len, (int64_t)(((16 - ps) & 15) >> 2));  // same phase: align both
+  else head = len;                                                    // different phase: scalar
+  for (int64_t e = threadIdx.x; e < head; e += blockDim.x) dst[e] = src[e];
+  const int64_t nv = (len - head) >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(src + head);
+  float4* d4 = reinterpret_cast<float4*>(dst + head);
+  for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) d4[v] = __ldcs(s4 + v);
+  for (int64_t e = head + 4 * nv + threadIdx.x; e < len; e += blockDim.x) dst[e] = src[e];
 }
 
 int pack_impl(const float* const* srcs, float* const* dsts, const int64_t* numels, int32_t count, float* fused,
               const float* cfused, int to_fused, cudaStream_t st) {
   if (count < 0 || !numels || (count > 0 && (to_fused ? !srcs : !dsts))) { set_error("bad pack arguments"); return MC_EINVAL; }
+  if (to_fused ? !fused : !cfused) { set_error("null fused buffer"); return MC_EINVAL; }
   int64_t base = 0;
   for (int32_t i0 = 0; i0 < count; i0 += PACK_MAX) {
     PackArgs a{};
     a.count = (int)imin(PACK_MAX, count - i0);
     a.to_fused = to_fused;
     a.off[0] = 0;
+    a.blk0[0] = 0;
     for (int i = 0; i < a.count; ++i) {
-      if (numels[i0 + i] < 0) { set_error("negative numel"); return MC_EINVAL; }
+      const int64_t m = numels[i0 + i];
+      if (m < 0) { set_error("negative numel"); return MC_EINVAL; }
+      if (m > 0 && (to_fused ? !srcs[i0 + i] : !dsts[i0 + i])) { set_error("null tensor pointer"); return MC_EINVAL; }
       if (to_fused) a.src[i] = srcs[i0 + i]; else a.dst[i] = dsts[i0 + i];
-      a.off[i + 1] = a.off[i] + numels[i0 + i];
+      a.off[i + 1] = a.off[i] + m;
+      const int64_t nb = a.blk0[i] + cdiv(m, PACK_CHUNK);
+      if (nb > 0x7fffffff) { set_error("merge stage too large for one launch"); return MC_EINVAL; }
+      a.blk0[i + 1] = (int32_t)nb;
     }
     a.fused = fused ? fused + base : nullptr;
     a.cfused = cfused ? cfused + base : nullptr;
-    const int64_t total = a.off[a.count];
-    if (total > 0) {
-      const unsigned grid = (unsigned)imax(1, imin(cdiv(total, 256), (int64_t)sm_count() * 8));
-      note_launch(); k_pack<<<grid, 256, 0, st>>>(a);
+    if (a.blk0[a.count] > 0) {
+      note_launch(); k_pack<<<(unsigned)a.blk0[a.count], 256, 0, st>>>(a);
       MC_LAUNCH_CHECK();
     }
-    base += total;
+    base += a.off[a.count];
   }
   return MC_OK;
 }

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/mergecomp.h"
 
 namespace mc {
@@ -31,7 +33,21 @@ inline bool is_sparse(int a) { return a == MC_TOPK || a == MC_RANDK || a == MC_D
 
 int64_t top_k_count(double sparsity, int64_t n);
 int fill_layout(const mc_spec* s, int64_t n, int64_t cap, mc_layout* L);
-int sm_count();
+int sm_count();  // of the current device (cached per device)
+
+// Dynamic shared memory above 48 KB is opted into per kernel AND per device: `mask` is the
+// call site's own set of devices already configured (one static per kernel instantiation),
+// so a process driving several GPUs configures each of them.
+template <class F>
+inline cudaError_t smem_optin(std::atomic<uint64_t>& mask, F* kernel, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 void set_error(const char* fmt, ...);
 void note_launch();  // counts kernel launches (mc_kernel_launches)
 
@@ -78,6 +94,50 @@ struct Philox {
       c0 = hi1 ^ c1 ^ a; c1 = lo1; c2 = hi0 ^ c3 ^ b; c3 = lo0;
     }
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+  }
+};
+
+// The same generator with its round keys (a_r, b_r) = (k0 + r W0, k1 + r W1) computed once on
+// the host and passed in the kernel parameters: the rounds then take the keys as constant-bank
+// operands (LOP3 ..., c[0x0][...]) instead of re-deriving the schedule for every block.
+struct PhiloxKS {
+  uint64_t a[10], b[10];
+  static PhiloxKS make(uint64_t k0, uint64_t k1) {
+    PhiloxKS ks;
+    for (int r = 0; r < 10; ++r) {
+      ks.a[r] = k0 + (uint64_t)r * 0x9E3779B97F4A7C15ull;
+      ks.b[r] = k1 + (uint64_t)r * 0xBB67AE8584CAA73Bull;
+    }
+    return ks;
+  }
+  __device__ __forceinline__ void block(uint64_t blk, uint64_t out[4]) const {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    uint64_t c0 = blk + 1, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint64_t lo0 = M0 * c0, hi0 = __umul64hi(M0, c0);
+      const uint64_t lo1 = M1 * c2, hi1 = __umul64hi(M1, c2);
+      c0 = hi1 ^ c1 ^ a[r]; c1 = lo1; c2 = hi0 ^ c3 ^ b[r]; c3 = lo0;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+  }
+  // J independent blocks blk0 + j*stride, rounds interleaved (J-way ILP on the IMAD chain)
+  template <int J>
+  __device__ __forceinline__ void blocks(uint64_t blk0, uint64_t stride, uint64_t (&out)[J][4]) const {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    uint64_t c0[J], c1[J], c2[J], c3[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) { c0[j] = blk0 + (uint64_t)j * stride + 1; c1[j] = c2[j] = c3[j] = 0; }
+#pragma unroll
+    for (int r = 0; r < 10; ++r)
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const uint64_t lo0 = M0 * c0[j], hi0 = __umul64hi(M0, c0[j]);
+        const uint64_t lo1 = M1 * c2[j], hi1 = __umul64hi(M1, c2[j]);
+        c0[j] = hi1 ^ c1[j] ^ a[r]; c1[j] = lo1; c2[j] = hi0 ^ c3[j] ^ b[r]; c3[j] = lo0;
+      }
+#pragma unroll
+    for (int j = 0; j < J; ++j) { out[j][0] = c0[j]; out[j][1] = c1[j]; out[j][2] = c2[j]; out[j][3] = c3[j]; }
   }
 };
 
@@ -467,7 +527,8 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a, cudaStream_t st);
+int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a, cudaStream_t st,
+                     const mc_layout* sparse = nullptr);
 
 int64_t bucket_ws_bytes(const mc_spec* s, int64_t n);
 int64_t sparse_ws_bytes(const mc_spec* s, int64_t n);
@@ -486,6 +547,7 @@ int encode_threshold(const EncodeArgs& a, float* out);
 int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks,
                       float* out, const Ctx& c);
 int decode_mean_sparse(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks,
-                       float* out, const Ctx& c);
+                       float* out, const Ctx& c, void* ws, int64_t ws_bytes);
+int64_t decode_sparse_ws_bytes(int64_t n, int nranks);
 
 }  // namespace mc

@@ -198,12 +198,9 @@ void launch_nodes(const SP& p, int64_t n, int64_t nodes, cudaStream_t st) {
       if (vec) k_sign_nodes<8, MOM, EF, true><<<grid, SW * 32, sm8, st>>>(p);
       else k_sign_nodes<8, MOM, EF, false><<<grid, SW * 32, sm8, st>>>(p);
     } else {
-      static bool cfg = false;  // idempotent (benign race)
-      if (!cfg) {
-        cudaFuncSetAttribute(k_sign_nodes<16, MOM, EF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
-        cudaFuncSetAttribute(k_sign_nodes<16, MOM, EF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
-        cfg = true;
-      }
+      static std::atomic<uint64_t> cfg_v{0}, cfg_s{0};
+      smem_optin(cfg_v, k_sign_nodes<16, MOM, EF, true>, sm16);  // a failure surfaces at the launch check
+      smem_optin(cfg_s, k_sign_nodes<16, MOM, EF, false>, sm16);
       if (vec) k_sign_nodes<16, MOM, EF, true><<<grid, SW * 32, sm16, st>>>(p);
       else k_sign_nodes<16, MOM, EF, false><<<grid, SW * 32, sm16, st>>>(p);
     }

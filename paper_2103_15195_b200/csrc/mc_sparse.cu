@@ -1629,11 +1629,8 @@ int encode_randk(const EncodeArgs& a, float* out) {
 #define MC_RANDK_WALK(DWV, RXV)                                                                                    \
   {                                                                                                               \
     const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2;                                                          \
-    static bool cfg = false; /* idempotent attribute set (benign race) */                                          \
-    if (!cfg) {                                                                                                   \
-      MC_API_CHECK(cudaFuncSetAttribute(k_randk_tables<DWV, RXV>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts)); \
-      cfg = true;                                                                                                 \
-    }                                                                                                             \
+    static std::atomic<uint64_t> cfg{0}; /* per device */                                                         \
+    MC_API_CHECK(smem_optin(cfg, k_randk_tables<DWV, RXV>, ts));                                                  \
     note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, expw, nwin, Lw, tables); \
     note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp, mid);                 \
     note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, mid, tg, tin, ctl);              \
@@ -1663,8 +1660,10 @@ int encode_randk(const EncodeArgs& a, float* out) {
   return MC_OK;
 }
 
+int64_t decode_sparse_ws_bytes(int64_t n, int nranks) { return a16(4 * (int64_t)nranks * (cdiv(n, DT) + 1)); }
+
 int decode_mean_sparse(const mc_spec* s, const mc_layout& L, const uint8_t* base, int64_t stride, int nranks, float* out,
-                       const Ctx& c) {
+                       const Ctx& c, void* ws, int64_t ws_bytes) {
   SD p{};
   p.base = base;
   p.stride = stride;
@@ -1674,19 +1673,18 @@ int decode_mean_sparse(const mc_spec* s, const mc_layout& L, const uint8_t* base
   p.out = out;
   p.err = c.err;
   p.algo = (uint32_t)s->algorithm;
-  // the tile-start table lives in a stream-ordered scratch allocation
-  const size_t bytes = 4 * (size_t)nranks * (size_t)(p.ntiles + 1);
-  void* scratch = nullptr;
-  if (cudaMallocAsync(&scratch, bytes, c.stream) != cudaSuccess) {
-    set_error("cudaMallocAsync(%zu) failed", bytes);
-    return MC_ECUDA;
+  // the per-(rank, tile) start table lives in the caller's workspace (no allocation here)
+  const int64_t need = decode_sparse_ws_bytes(L.n, nranks);
+  if (!ws || ws_bytes < need) {
+    set_error("sparse decode workspace %lld < required %lld (mc_decode_workspace_bytes)", (long long)ws_bytes,
+              (long long)need);
+    return MC_EWORKSPACE;
   }
-  p.starts = static_cast<uint32_t*>(scratch);
+  p.starts = static_cast<uint32_t*>(ws);
   const int64_t maxcap = L.cap > 0 ? L.cap : L.n;
   dim3 g1((unsigned)imax(1, imin(cdiv(maxcap + 1, 256), (int64_t)sm_count() * 4)), (unsigned)nranks);
   note_launch(); k_sparse_starts<<<g1, 256, 0, c.stream>>>(p);
   note_launch(); k_sparse_tiles<<<(unsigned)p.ntiles, 256, 0, c.stream>>>(p);
-  cudaFreeAsync(scratch, c.stream);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }

@@ -61,35 +61,84 @@ def allgather_fixed(payload: torch.Tensor, out: Optional[torch.Tensor] = None, g
     return (out, stride, work) if async_op else (out, stride)
 
 
-def read_count(payload: torch.Tensor) -> torch.Tensor:
-    """n_idx field of the device header (u32 at byte 16) as an int64 tensor on the payload's device."""
-    return payload[16:20].view(torch.int32).to(torch.int64)
+def allreduce_mean_(x: torch.Tensor, group=None, async_op: bool = False):
+    """Uncompressed data-parallel baseline (BASELINE config 5's comparator; reference
+    ``cli._collective_for``: identity / fp16 -> allreduce, cli.py:107-109): in-place
+    ``all_reduce(SUM)`` of the fp32 gradients, then ``/ f32(world)``.  The ring / NVLS
+    summation order differs from ``aggregate``'s rank order for world >= 3, so it is a
+    throughput comparator, not a parity target.  With ``async_op`` the
+    division is left to the caller after ``work.wait()``; returns the work handle (or None)."""
+    _, n = world(group)
+    if n == 1:
+        return None
+    if x.is_cuda and dist.get_backend(group) == "gloo":  # several ranks on one GPU (tests)
+        host = x.cpu()
+        dist.all_reduce(host, group=group)
+        x.copy_(host)
+        work = None
+    else:
+        work = dist.all_reduce(x, group=group, async_op=async_op)
+    if work is None or not async_op:
+        x.div_(float(n))
+        return None
+    return work
 
 
-def _repack(payload: torch.Tensor, count: int, cap_out: int, cap_in: Optional[int]) -> torch.Tensor:
-    """Re-lay a sparse payload [hdr | idx[cap_in] | val[cap_in]] with capacity cap_out >= count."""
+def read_count(payload: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """n_idx field of the device header (u32 at byte 16) as an int64 tensor on the payload's
+    device (into ``out`` when given: no allocation)."""
+    v = payload[16:20].view(torch.int32)
+    if out is None:
+        return v.to(torch.int64)
+    out.copy_(v)
+    return out
+
+
+def _repack(payload: torch.Tensor, count: int, cap_out: int, cap_in: Optional[int],
+            out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Re-lay a sparse payload [hdr | idx[cap_in] | val[cap_in]] with capacity cap_out >= count
+    (into a view of ``out`` when given: no allocation, only device copies)."""
     if cap_in is None:
         cap_in = int(payload[28:32].view(torch.int32).cpu().item())
-    out = torch.zeros(HDR + 2 * _a16(4 * cap_out), dtype=torch.uint8, device=payload.device)
+    size = HDR + 2 * _a16(4 * cap_out)
+    if out is None:
+        out = torch.zeros(size, dtype=torch.uint8, device=payload.device)
+    else:
+        out = out[:size]
     out[:HDR].copy_(payload[:HDR])
-    out[28:32].copy_(torch.tensor([cap_out], dtype=torch.int32).view(torch.uint8).to(payload.device))
+    out[28:32].view(torch.int32).fill_(cap_out)
     out[HDR: HDR + 4 * count].copy_(payload[HDR: HDR + 4 * count])
     v_in, v_out = HDR + _a16(4 * cap_in), HDR + _a16(4 * cap_out)
     out[v_out: v_out + 4 * count].copy_(payload[v_in: v_in + 4 * count])
     return out
 
 
-def allgather_variable(payload: torch.Tensor, group=None) -> tuple[torch.Tensor, int, list[int]]:
-    """Two-phase gather of sparse payloads with data-dependent counts.
-    Returns (gathered, stride, counts)."""
+def allgather_variable(payload: torch.Tensor, group=None, cap_in: Optional[int] = None,
+                       bufs: Optional[dict] = None) -> tuple[torch.Tensor, int, list[int]]:
+    """Two-phase gather of sparse payloads with data-dependent counts (NCCL / gloo path).
+    Returns (gathered, stride, counts).
+
+    One host synchronisation per call — the padded size of the second gather is the max
+    count, which the host must know to size the collective.  With ``cap_in`` (the payload's
+    known capacity) and ``bufs`` (persistent ``counts`` int64[world], ``cnt`` int64[1],
+    ``mine`` u8[>= payload bytes] and ``gather`` u8[>= world * payload bytes]) a step
+    allocates nothing.  The zero-sync variable-size exchange is the peer push
+    (GradSync.use_peer_exchange: the push kernel reads n_idx on the device)."""
     r, n = world(group)
-    cnt = read_count(payload)
     if n == 1:
-        return payload, payload.numel(), [int(cnt.item())]
-    counts = torch.empty(n, dtype=torch.int64, device=payload.device)
+        return payload, payload.numel(), [int(read_count(payload).item())]
+    if bufs is None:
+        cnt = read_count(payload)
+        counts = torch.empty(n, dtype=torch.int64, device=payload.device)
+    else:
+        cnt = read_count(payload, bufs["cnt"])
+        counts = bufs["counts"]
     _gather_into(counts, cnt.reshape(1), group)
     counts_h = [int(v) for v in counts.cpu().tolist()]  # host sync: the padded size depends on it
     cap = max(max(counts_h), 1)
-    mine = _repack(payload, counts_h[r], cap, None)
-    gathered, stride = allgather_fixed(mine, group=group)
+    mine = _repack(payload, counts_h[r], cap, cap_in, None if bufs is None else bufs["mine"])
+    if bufs is None:
+        gathered, stride = allgather_fixed(mine, group=group)
+    else:
+        gathered, stride = allgather_fixed(mine, bufs["gather"][:n * mine.numel()], group=group)
     return gathered, stride, counts_h

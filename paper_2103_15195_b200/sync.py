@@ -22,6 +22,7 @@ all on a dedicated side stream — the FIFO channel of the reference simulator
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import Optional, Sequence, Union
 
@@ -42,6 +43,7 @@ class _Group:
     gather: Optional[torch.Tensor]
     residual: Optional[torch.Tensor]
     momentum: Optional[torch.Tensor]
+    xbufs: Optional[dict] = None  # threshold over NCCL: persistent counts / re-pack buffers
 
     @property
     def n(self) -> int:
@@ -114,13 +116,19 @@ class GradSync:
             n = end - start
             L = _native.layout(self.cspec, n)
             payload = torch.zeros(L.bytes, dtype=torch.uint8, device=self.device)
-            gather = None
-            if self.world > 1 and self.spec.algorithm != "threshold":
+            gather = xbufs = None
+            if self.world > 1:
                 gather = torch.empty(self.world * L.bytes, dtype=torch.uint8, device=self.device)
+                if self.spec.algorithm == "threshold":  # padded to the step's max count, in place
+                    xbufs = {"cnt": torch.zeros(1, dtype=torch.int64, device=self.device),
+                             "counts": torch.zeros(self.world, dtype=torch.int64, device=self.device),
+                             "mine": torch.zeros(L.bytes, dtype=torch.uint8, device=self.device),
+                             "gather": gather}
             plan.append(_Group(
                 start, end, L, payload, gather,
                 torch.zeros(n, dtype=torch.float64, device=self.device) if ef else None,
                 torch.zeros(n, dtype=torch.float32, device=self.device) if mom else None,
+                xbufs,
             ))
         self._plans[key] = plan
         return plan
@@ -186,7 +194,8 @@ class GradSync:
             ev[1].record(self.stream)
             self.probe[1].append(ev)
         if self.spec.algorithm == "threshold":
-            gathered, stride, _ = exchange.allgather_variable(grp.payload, group=self.pg)
+            gathered, stride, _ = exchange.allgather_variable(grp.payload, group=self.pg, cap_in=grp.layout.cap,
+                                                              bufs=grp.xbufs)
         else:
             gathered, stride = exchange.allgather_fixed(grp.payload, grp.gather, group=self.pg)
         device_decode_mean(self.spec, gathered, stride, self.world, grp.n, x, self.err, stream=self.stream,
@@ -213,7 +222,9 @@ class GradSync:
         part = self.partition if partition is None else self._resolve(partition)
         self.partition = part
         plan = self._plan(part)
-        need = max(_native.workspace_bytes(self.cspec, grp.n) for grp in plan)
+        need = max(max(_native.workspace_bytes(self.cspec, grp.n),
+                       _native.lib().mc_decode_workspace_bytes(ctypes.byref(self.cspec), grp.n, self.world))
+                   for grp in plan)
         ws = _WS.get(self.device, need, self.stream)  # sized before capture: the graph keeps these pointers
         graph = torch.cuda.CUDAGraph()
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
@@ -224,6 +235,25 @@ class GradSync:
 
     def drop_graph(self) -> None:
         self._graph = None
+
+    # ------------------------------------------------------------ dense baseline
+    def use_dense_allreduce(self) -> None:
+        """Replace compress -> allgather -> decode by the uncompressed baseline of BASELINE
+        config 5: per group one NCCL all_reduce(SUM) of the fp32 slice in place, then / N
+        (exchange.allreduce_mean_).  The codec and its state are bypassed; groups are
+        pipelined (all-reduce g+1 is issued while g's division waits)."""
+        self._dense = True
+
+    def _step_dense(self, plan) -> None:
+        pending = []
+        for grp in plan:
+            x = self.flat[grp.start:grp.end]
+            work = exchange.allreduce_mean_(x, group=self.pg, async_op=True)
+            pending.append((x, work))
+        for x, work in pending:
+            if work is not None:
+                work.wait()
+                x.div_(float(self.world))
 
     # ------------------------------------------------------------ allgather over peer memory
     def use_peer_exchange(self, backend: str = "ipc") -> None:
@@ -236,41 +266,76 @@ class GradSync:
         straight into its slot of every rank's buffer and releases their flags when done.
         Double buffering is enough: a rank pushes epoch e+2 into the buffer a peer read at
         epoch e only after that peer's epoch-(e+1) push, which its stream issued after its
-        decode of epoch e.  Fixed-size payloads (not threshold)."""
+        decode of epoch e.  Threshold payloads (data-dependent count) get capacity-n slots
+        and the push moves only the header and the first n_idx entries, read on the device:
+        the variable-size exchange with no host round trip."""
         if self.world < 2:
             raise ValueError("the peer exchange needs more than one rank")
-        if self.spec.algorithm == "threshold":
-            raise ValueError("threshold payloads are variable-size: use the NCCL exchange")
         if backend not in ("ipc", "symm"):
             raise ValueError(f"unknown peer backend {backend!r}")
         self._peer = {"backend": backend, "groups": {}, "epoch": 0}
 
+    PROBE_MAGIC = 0x5EED0000
+
+    def _all_ok(self, ok: int) -> bool:
+        t = torch.tensor([ok], dtype=torch.int32, device=self.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN, group=self.pg)
+        return int(t.item()) == 1
+
     def try_peer_exchange(self, backend: str = "ipc") -> bool:
-        """Collective probe (every rank must call it): map a small buffer of every rank; if
-        that works everywhere, switch this GradSync to the peer exchange and return True,
-        else keep the NCCL allgather.  The collectives run on all ranks whatever fails
-        locally, so a failed probe cannot deadlock."""
-        if self.world < 2 or self.spec.algorithm == "threshold":
+        """Collective probe (every rank must call it) that proves the peer path before any
+        encode kernel pushes through it, else keeps the NCCL allgather:
+
+        1. map a small probe buffer of every rank (CUDA IPC handles);
+        2. enable P2P access from this device to every peer's device (mc_peer_enable —
+           opening an IPC handle does not grant the importing device access);
+        3. one kernel on THIS device stores ``magic | rank`` into this rank's slot of every
+           rank's probe buffer (mc_peer_probe), then each rank reads back its own buffer and
+           checks that every peer's store arrived.
+
+        A step is only attempted when every rank passed the previous one (MIN all-reduce),
+        so a device pair without P2P never reaches a kernel store (which would fault the
+        context instead of falling back), and every collective runs on all ranks whatever
+        fails locally, so a failed probe cannot deadlock."""
+        if self.world < 2:
             return False
-        ok = 1
+        from .compressors import _stream_ptr
+
+        lib = _native.lib()
         self._peer = {"backend": backend, "groups": {}, "epoch": 0}
-        probe = torch.zeros(16, dtype=torch.int32, device=self.device)
+        probe = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+        mapped = []
+        ok = 1
         try:
             if backend == "symm":
                 raise RuntimeError("probe covers the IPC backend only")
             from torch.multiprocessing.reductions import reduce_tensor
 
             handles = [None] * self.world
+            torch.cuda.synchronize(self.device)
             torch.distributed.all_gather_object(handles, reduce_tensor(probe), group=self.pg)
             for j, (fn, args) in enumerate(handles):
-                if j != self.rank:
-                    self._peer.setdefault("mapped", []).append(fn(*args))
+                mapped.append(probe if j == self.rank else fn(*args))
+            for t in mapped:
+                _native.check(lib.mc_peer_enable(self.device.index, t.device.index), "mc_peer_enable")
         except Exception:  # noqa: BLE001 - fall back to NCCL on every rank
             ok = 0
-        t = torch.tensor([ok], dtype=torch.int32, device=self.device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN, group=self.pg)
-        if int(t.item()) == 1:
-            return True
+        if self._all_ok(ok):
+            try:
+                dsts = (ctypes.c_void_p * self.world)(*[t.data_ptr() + 4 * self.rank for t in mapped])
+                s = torch.cuda.current_stream(self.device)
+                _native.check(lib.mc_peer_probe(dsts, self.world, self.PROBE_MAGIC | self.rank, _stream_ptr(s)),
+                              "mc_peer_probe")
+                torch.cuda.synchronize(self.device)
+            except Exception:  # noqa: BLE001
+                ok = 0
+            torch.distributed.barrier(group=self.pg)  # every rank's stores are complete
+            if ok:
+                got = [int(v) & 0xFFFFFFFF for v in probe.cpu().tolist()]
+                ok = int(got == [self.PROBE_MAGIC | j for j in range(self.world)])
+            if self._all_ok(ok):
+                self._peer["mapped"] = mapped
+                return True
         self._peer = None
         return False
 
@@ -292,6 +357,8 @@ class GradSync:
                 ptrs.append(t.data_ptr())
             else:
                 peer = fn(*args)  # opens the IPC handle: a tensor over rank j's memory
+                # the handle is opened under rank j's device: grant THIS device's kernels access
+                _native.check(_native.lib().mc_peer_enable(self.device.index, peer.device.index), "mc_peer_enable")
                 keep.append(peer)
                 ptrs.append(peer.data_ptr())
         return ptrs
@@ -366,7 +433,9 @@ class GradSync:
         plan = self._plan(part)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
-            if getattr(self, "_peer", None) is not None:
+            if getattr(self, "_dense", False):
+                self._step_dense(plan)
+            elif getattr(self, "_peer", None) is not None:
                 self._step_peer(plan, part.boundaries)
             elif self.world > 1 and self.spec.algorithm != "threshold" and len(plan) > 1:
                 pending = []

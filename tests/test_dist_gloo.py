@@ -63,6 +63,24 @@ def _worker(rank, world, port, q):
             val = blk[voff:voff + 4 * counts[r]].view(torch.float32)
             assert idx.tolist() == [3 * i + r for i in range(counts[r])]
             assert val.tolist() == [float(i + 100 * r) for i in range(counts[r])]
+        # the same, through persistent buffers (the GradSync NCCL path: no allocation)
+        bufs = {"cnt": torch.zeros(1, dtype=torch.int64), "counts": torch.zeros(world, dtype=torch.int64),
+                "mine": torch.zeros(pay.numel(), dtype=torch.uint8),
+                "gather": torch.zeros(world * pay.numel(), dtype=torch.uint8)}
+        g2, s2, c2 = exchange.allgather_variable(pay, cap_in=50, bufs=bufs)
+        assert c2 == counts and s2 == stride and torch.equal(g2, gathered)
+        assert g2.data_ptr() == bufs["gather"].data_ptr()
+        # dense baseline: in-place sum then / world, equal to aggregate of identity payloads
+        x = torch.linspace(-1, 1, 101, dtype=torch.float32) * (rank + 1) / 3
+        ref = (torch.linspace(-1, 1, 101, dtype=torch.float32) / 3 + torch.linspace(-1, 1, 101) * 2 / 3) / 2.0
+        exchange.allreduce_mean_(x)
+        assert torch.equal(x, ref)
+        y = torch.full((7,), float(rank))
+        work = exchange.allreduce_mean_(y, async_op=True)
+        if work is not None:
+            work.wait()
+            y.div_(2.0)
+        assert torch.equal(y, torch.full((7,), 0.5))
         assert exchange.world() == (rank, world)
         q.put((rank, "ok"))
     except Exception as exc:  # noqa: BLE001

@@ -43,7 +43,13 @@ def _rank(rank, world, port, kw, q, peer=False):
         torch.cuda.set_device(0)
         prof = gradsets.profile("tiny40")
         sync = GradSync(CompressorSpec(**kw), prof, partition=Partition(prof.n_tensors, (7, 30)), root_seed=3)
-        if peer:
+        if peer == "dense":  # the uncompressed all_reduce baseline (config 5's comparator)
+            sync.use_dense_allreduce()
+        elif peer == "probe":  # the production entry: store-then-readback probe, then push
+            if not sync.try_peer_exchange():
+                q.put((rank, "peer probe failed"))
+                return
+        elif peer:
             try:
                 sync.use_peer_exchange()
                 sync._peer_group(sync.partition.boundaries, 0, sync._plan(sync.partition)[0])
@@ -53,7 +59,20 @@ def _rank(rank, world, port, kw, q, peer=False):
         outs = []
         for it in range(3):
             sync.flat.copy_(torch.from_numpy(gradsets.synthetic_gradients("tiny40", it, rank)))
-            sync.step()
+            torch.cuda.synchronize()
+            if peer in (True, "probe") and it > 0:  # the peer step: no host synchronisation, no allocation
+                a0 = torch.cuda.memory_stats(0).get("allocation.all.allocated", 0)
+                torch.cuda.set_sync_debug_mode("error")
+                try:
+                    sync.step()
+                finally:
+                    torch.cuda.set_sync_debug_mode("default")
+                a1 = torch.cuda.memory_stats(0).get("allocation.all.allocated", 0)
+                if a1 != a0:
+                    q.put((rank, f"peer step allocated {a1 - a0} blocks"))
+                    return
+            else:
+                sync.step()
             torch.cuda.synchronize()
             sync.check()
             outs.append(sync.flat.cpu().numpy().copy())
@@ -64,11 +83,16 @@ def _rank(rank, world, port, kw, q, peer=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("peer", [False, True], ids=["nccl-path", "peer-push"])
+@pytest.mark.parametrize("peer", [False, True, "probe"], ids=["nccl-path", "peer-push", "peer-probe"])
 @pytest.mark.parametrize("kw", SPECS, ids=lambda k: k["algorithm"])
 def test_two_ranks_match_oracle(kw, peer):
-    """peer-push: the allgather replaced by mc_encode_push into torch symmetric-memory
-    buffers of both ranks (skipped where symmetric memory cannot be set up)."""
+    """peer-push: the allgather replaced by mc_encode_push into CUDA-IPC-mapped buffers of
+    both ranks; peer-probe: the same reached through try_peer_exchange (peer access enabled,
+    one store-then-readback probe kernel per rank) as bench.py does."""
+    _run_pair(kw, peer)
+
+
+def _run_pair(kw, peer):
     import torch.multiprocessing as mp
 
     import mergecomp_oracle as O
@@ -79,8 +103,6 @@ def test_two_ranks_match_oracle(kw, peer):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    if peer and kw["algorithm"] == "threshold":
-        pytest.skip("threshold payloads are variable-size (NCCL exchange only)")
     procs = [ctx.Process(target=_rank, args=(r, 2, port, kw, q, peer)) for r in range(2)]
     for p in procs:
         p.start()
@@ -105,3 +127,10 @@ def test_two_ranks_match_oracle(kw, peer):
             for r in (0, 1):
                 got = res[r][it][a:b]
                 assert np.array_equal(got.view(np.uint32), mean.view(np.uint32)), (spec.algorithm, it, gi, r)
+
+
+
+def test_two_ranks_dense_allreduce_equals_identity_aggregate():
+    """Two ranks: all_reduce(SUM) / 2 is bitwise the reference aggregate of identity payloads
+    ((0 + a) + b) / f32(2) — commutative for two terms (for >= 3 ranks only a tolerance)."""
+    _run_pair(dict(algorithm="identity"), "dense")

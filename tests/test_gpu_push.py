@@ -10,14 +10,14 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8", "dgc_lite", "qsgd", "signsgd", "fp16"])
+@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8", "dgc_lite", "qsgd", "signsgd", "fp16", "threshold"])
 @pytest.mark.parametrize("nranks", [2, 4])
 def test_encode_push_equals_allgather(algo, nranks):
     from paper_2103_15195_b200 import _native
     from paper_2103_15195_b200 import compressors as C
     from paper_2103_15195_b200.spec import CompressorSpec
 
-    spec = CompressorSpec(algo, sparsity=0.999)
+    spec = CompressorSpec(algo, sparsity=0.999, threshold=2e-3)
     n = 1_000_003 if algo not in ("efsignsgd", "onebit", "int8") else 1_048_576 + 512 * 7 + 13
     L = _native.layout(spec.to_c(), n)
     stride = (L.bytes + 15) // 16 * 16
@@ -41,7 +41,15 @@ def test_encode_push_equals_allgather(algo, nranks):
             C.device_encode(spec, grads[r] * epoch, res_b[r], None, 1000 * epoch + r, out=ref[r * stride:r * stride + L.bytes])
         torch.cuda.synchronize()
         for j in range(nranks):
-            assert torch.equal(gather[j], ref), (algo, nranks, epoch, j)
+            if algo == "threshold":  # the push moves header + the first n_idx entries only
+                for r in range(nranks):
+                    a, b = gather[j][r * stride:(r + 1) * stride], ref[r * stride:(r + 1) * stride]
+                    cnt = int(b[16:20].view(torch.int32).item())
+                    assert 0 < cnt < n and torch.equal(a[:32], b[:32])
+                    for off in (L.off_idx, L.off_val):
+                        assert torch.equal(a[off:off + 4 * cnt], b[off:off + 4 * cnt]), (epoch, j, r)
+            else:
+                assert torch.equal(gather[j], ref), (algo, nranks, epoch, j)
         if ef:
             for r in range(nranks):
                 assert torch.equal(res_a[r].view(torch.int64), res_b[r].view(torch.int64))
@@ -55,3 +63,29 @@ def test_encode_push_equals_allgather(algo, nranks):
         assert int(err.item()) == 0
         for o in outs[1:]:
             assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32))
+
+
+@pytest.mark.parametrize("case", ["ragged", "resnet50"])
+def test_merge_stage_pack_unpack(case):
+    """K1 / K11 (trainer.py:344-348 as a copy): mc_pack == torch.cat, mc_unpack its inverse,
+    for ragged sizes (zero-length tensors, 8192-element chunk edges, every 16-byte phase of
+    source vs fused offset) and the 161 ResNet-50 tensors (> 128: one launch since PACK_MAX=512)."""
+    from paper_2103_15195_b200 import gradsets, merge
+
+    if case == "ragged":  # empty tensors, 8192-element chunk edges
+        sizes = [1, 3, 4, 5, 8191, 8192, 8193, 0, 17, 100_000]
+    else:
+        sizes = list(gradsets.sizes("resnet50_161"))
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(5)
+    # sub-views at odd element offsets make the sources' 16-byte phase differ from the fused one
+    backing = [torch.randn(n + 3, generator=g).to(dev) for n in sizes]
+    srcs = [b[1 + (i % 3): 1 + (i % 3) + n] for i, (b, n) in enumerate(zip(backing, sizes))]
+    fused = merge.pack(srcs)
+    ref = torch.cat([s.reshape(-1) for s in srcs])
+    assert torch.equal(fused, ref)
+    outs = [torch.full((n,), float("nan"), device=dev) for n in sizes]
+    merge.unpack(fused * 2, outs)
+    torch.cuda.synchronize()
+    for o, s in zip(outs, srcs):
+        assert torch.equal(o, s * 2)
