@@ -235,3 +235,33 @@ def test_serialize_deserialize_roundtrip_on_device(algo, C):
         C.device_deserialize(spec, raw + b"\0")
     with pytest.raises(ValueError, match="unknown algorithm id"):
         C.device_deserialize(spec, bytes([99]) + raw[1:])
+
+
+@pytest.mark.parametrize("algo,bucket", [("efsignsgd", 512), ("efsignsgd", 384), ("onebit", 512), ("onebit", 128),
+                                         ("signsgd", 512), ("signum", 512)])
+@pytest.mark.parametrize("nranks", [2, 3, 5, 8, 9])
+def test_sign_decode_mean_many_ranks_matches_oracle(algo, bucket, nranks, C):
+    """decode_mean over 2..9 stacked sign payloads (3..8 take the per-bucket table kernel,
+    2 and 9 the per-element loop) against the oracle's rank-ordered aggregate, bit for bit.
+    Ranks differ in magnitude by up to 10^4 so the f32 addition order is visible; the group
+    length leaves a partial word and a partial bucket; some buckets are all zero."""
+    import torch
+
+    import mergecomp_oracle as O
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    spec = CompressorSpec(algo, bucket_size=bucket)
+    n = 200_003
+    rng = np.random.default_rng(nranks * 1000 + bucket)
+    pays_d, pays_o = [], []
+    for r in range(nranks):
+        g = (rng.standard_normal(n) * (1e-3 * 10.0 ** ((r % 5) - 2))).astype(np.float32)
+        g[4096:4096 + 3 * bucket] = 0.0  # all-zero buckets (sign bit 1, scale 0)
+        g[7] = -0.0
+        p, _ = C.encode(spec, torch.from_numpy(g).cuda(), None, seed=0)
+        q, _ = O.encode(spec, g, None, seed=0)
+        pays_d.append(p)
+        pays_o.append(q)
+    mean_d = C.aggregate(spec, pays_d).cpu().numpy()
+    mean_o = O.aggregate(spec, pays_o)
+    _eq_bits(mean_d, mean_o, f"{algo} B={bucket} N={nranks} mean")
