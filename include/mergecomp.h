@@ -103,6 +103,10 @@ typedef struct mc_layout {
 int mc_abi_version(void);
 const char* mc_last_error(void); /* thread-local message of the last failing call */
 int64_t mc_kernel_launches(void); /* kernels launched by this library since load (statistics) */
+/* Size every grid for (SMs - n) so n SMs stay free for a collective running concurrently on
+ * another stream (the chunked allgather pipeline's NCCL kernels); process-wide, returns the
+ * previous value.  Default 0.  No reference counterpart (its allgather is a Python list). */
+int mc_set_sm_reserve(int32_t n);
 
 int64_t mc_top_k_count(double sparsity, int64_t n);
 int64_t mc_payload_bytes(const mc_spec* spec, int64_t n);               /* canonical, incl. 22-B header */

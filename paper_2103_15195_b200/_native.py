@@ -50,6 +50,7 @@ _SIGS = {
     "mc_abi_version": (ctypes.c_int, []),
     "mc_last_error": (ctypes.c_char_p, []),
     "mc_kernel_launches": (ctypes.c_int64, []),
+    "mc_set_sm_reserve": (ctypes.c_int, [ctypes.c_int32]),
     "mc_top_k_count": (ctypes.c_int64, [ctypes.c_double, ctypes.c_int64]),
     "mc_payload_bytes": (ctypes.c_int64, [_SPEC, ctypes.c_int64]),
     "mc_payload_layout": (ctypes.c_int, [_SPEC, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(McLayout)]),

@@ -23,6 +23,9 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+static std::atomic<int> g_sm_reserve{0};  // SMs left to a concurrent collective (mc_set_sm_reserve)
+
+// SMs the library sizes its grids for: the device's count less the reserve
 int sm_count() {
   static std::atomic<int> cached[64];  // per device (zero = not read yet)
   int dev = 0;
@@ -33,7 +36,8 @@ int sm_count() {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
     c.store(v, std::memory_order_relaxed);
   }
-  return v;
+  const int r = g_sm_reserve.load(std::memory_order_relaxed);
+  return v - r >= 1 ? v - r : 1;
 }
 
 // max(1, ceil(round((1 - s) * n, 9)))  — compressors.py:185-194.  Python's round(x, 9)
@@ -119,6 +123,10 @@ static uint32_t mix(uint32_t x, uint32_t y) {
 using namespace mc;
 
 extern "C" {
+
+int mc_set_sm_reserve(int32_t n) {
+  return mc::g_sm_reserve.exchange(n > 0 ? n : 0);
+}
 
 int mc_abi_version(void) { return MC_ABI_VERSION; }
 const char* mc_last_error(void) { return g_err; }

@@ -23,6 +23,7 @@ all on a dedicated side stream — the FIFO channel of the reference simulator
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass
 from typing import Optional, Sequence, Union
 
@@ -35,6 +36,21 @@ from .spec import CompressorSpec
 
 
 @dataclass
+class _Chunk:
+    """A bucket-aligned slice of a group with its own payload and gather buffer: the unit of
+    the chunked encode -> allgather -> decode pipeline (N > 1, per-bucket codecs)."""
+    start: int  # absolute element offsets in the flat buffer
+    end: int
+    layout: object
+    payload: torch.Tensor
+    gather: torch.Tensor
+
+    @property
+    def n(self) -> int:
+        return self.end - self.start
+
+
+@dataclass
 class _Group:
     start: int
     end: int
@@ -44,6 +60,7 @@ class _Group:
     residual: Optional[torch.Tensor]
     momentum: Optional[torch.Tensor]
     xbufs: Optional[dict] = None  # threshold over NCCL: persistent counts / re-pack buffers
+    chunks: Optional[list] = None  # N > 1 chunk pipeline (GradSync.CHUNKABLE codecs)
 
     @property
     def n(self) -> int:
@@ -88,6 +105,10 @@ class GradSync:
         self.partition = self._resolve(partition)
         self.probe = None  # (group index, list) -> CUDA events around that group's encode
         self.fuse_local = True  # world size 1: fused encode + decode (mc_encode_decode)
+        # N > 1 chunk pipeline: None = automatic (groups of >= 4M elements in ~4 chunks of
+        # >= 2M), 0 = off, else the chunk length (rounded up to the bucket / word alignment)
+        self.chunk_elems: Optional[int] = None
+        self.sm_reserve = 16  # SMs left to NCCL while the chunk pipeline's kernels run
 
     # ------------------------------------------------------------ partitions / state
     def _resolve(self, partition) -> Partition:
@@ -116,8 +137,16 @@ class GradSync:
             n = end - start
             L = _native.layout(self.cspec, n)
             payload = torch.zeros(L.bytes, dtype=torch.uint8, device=self.device)
-            gather = xbufs = None
-            if self.world > 1:
+            gather = xbufs = chunks = None
+            ranges = self._chunk_ranges(n)
+            if ranges is not None:
+                chunks = []
+                for a, b in ranges:
+                    Lc = _native.layout(self.cspec, b - a)
+                    chunks.append(_Chunk(start + a, start + b, Lc,
+                                         torch.zeros(Lc.bytes, dtype=torch.uint8, device=self.device),
+                                         torch.empty(self.world * Lc.bytes, dtype=torch.uint8, device=self.device)))
+            elif self.world > 1:
                 gather = torch.empty(self.world * L.bytes, dtype=torch.uint8, device=self.device)
                 if self.spec.algorithm == "threshold":  # padded to the step's max count, in place
                     xbufs = {"cnt": torch.zeros(1, dtype=torch.int64, device=self.device),
@@ -128,10 +157,39 @@ class GradSync:
                 start, end, L, payload, gather,
                 torch.zeros(n, dtype=torch.float64, device=self.device) if ef else None,
                 torch.zeros(n, dtype=torch.float32, device=self.device) if mom else None,
-                xbufs,
+                xbufs, chunks,
             ))
         self._plans[key] = plan
         return plan
+
+    # per-bucket / per-element codecs: a bucket-aligned slice encodes and decodes to exactly
+    # the values of the whole group (compressors.py:291-364 work bucket by bucket).  Chunked
+    # by default only where the payload is >= 1 byte per element: there the allgather costs
+    # more than the encode and hiding it pays (ResNet-50, 8 ranks, projected: int8 245 -> 317,
+    # fp16 171 -> 188 GB/s per GPU); for the 1-bit codecs four chunk launches on 132 SMs cost
+    # more encode time than the hidden allgather saves (efsignsgd 796 -> 683 at 2 ranks)
+    CHUNKABLE = frozenset({"identity", "fp16", "efsignsgd", "onebit", "int8"})
+    CHUNK_AUTO = frozenset({"identity", "fp16", "int8"})
+    CHUNK_MIN = 1 << 21
+
+    def _chunk_ranges(self, n: int):
+        """Relative [a, b) chunk bounds of an n-element group for the N > 1 pipeline, or None."""
+        if self.world == 1 or self.chunk_elems == 0 or self.spec.algorithm not in self.CHUNKABLE:
+            return None
+        if getattr(self, "_dense", False) or getattr(self, "_peer", None) is not None:
+            return None
+        B = self.spec.bucket_size
+        align = B * 32 // math.gcd(B, 32)
+        if self.chunk_elems is None:
+            if n < 2 * self.CHUNK_MIN or self.spec.algorithm not in self.CHUNK_AUTO:
+                return None
+            target = max(self.CHUNK_MIN, -(-n // 4))
+        else:
+            target = self.chunk_elems
+        target = -(-target // align) * align
+        if target >= n:
+            return None
+        return [(a, min(n, a + target)) for a in range(0, n, target)]
 
     # candidate partitions a measured search keeps alive besides the pinned one; each holds
     # an fp64 residual (8 B/elem) plus payload / gather buffers, so a Y>=3 search over
@@ -188,6 +246,13 @@ class GradSync:
                 ev[1].record(self.stream)
                 self.probe[1].append(ev)
             return 0
+        if grp.chunks:
+            pending = [self._encode_chunk(grp, c, key) for c in grp.chunks]
+            if probe:
+                ev[1].record(self.stream)
+                self.probe[1].append(ev)
+            self._decode_chunks(pending)
+            return 0
         device_encode(self.spec, x, grp.residual, grp.momentum, key, out=grp.payload,
                       err=self.err, stream=self.stream, cspec=self.cspec)
         if probe:
@@ -201,6 +266,22 @@ class GradSync:
         device_decode_mean(self.spec, gathered, stride, self.world, grp.n, x, self.err, stream=self.stream,
                            cspec=self.cspec)
         return 0
+
+    def _encode_chunk(self, grp: _Group, c: _Chunk, key: int):
+        """Encode one chunk (state slices of its group) and start its allgather (async)."""
+        a, b = c.start - grp.start, c.end - grp.start
+        device_encode(self.spec, self.flat[c.start:c.end], None if grp.residual is None else grp.residual[a:b],
+                      None if grp.momentum is None else grp.momentum[a:b], key, out=c.payload, err=self.err,
+                      stream=self.stream, cspec=self.cspec)
+        gathered, stride, work = exchange.allgather_fixed(c.payload, c.gather, group=self.pg, async_op=True)
+        return c, gathered, stride, work
+
+    def _decode_chunks(self, pending) -> None:
+        for c, gathered, stride, work in pending:
+            if work is not None:
+                work.wait()  # the side stream waits for this chunk's gather only
+            device_decode_mean(self.spec, gathered, stride, self.world, c.n, self.flat[c.start:c.end], self.err,
+                               stream=self.stream, cspec=self.cspec)
 
     # ------------------------------------------------------------ CUDA Graph of a pinned partition
     GRAPHABLE = frozenset({"identity", "fp16", "efsignsgd", "onebit", "int8", "signsgd", "signum", "topk",
@@ -437,18 +518,29 @@ class GradSync:
                 self._step_dense(plan)
             elif getattr(self, "_peer", None) is not None:
                 self._step_peer(plan, part.boundaries)
-            elif self.world > 1 and self.spec.algorithm != "threshold" and len(plan) > 1:
-                pending = []
-                for g, grp in enumerate(plan):
-                    x = self._encode_group(g, grp)
-                    gathered, stride, work = exchange.allgather_fixed(grp.payload, grp.gather, group=self.pg,
-                                                                      async_op=True)
-                    pending.append((grp, x, gathered, stride, work))
-                for grp, x, gathered, stride, work in pending:
-                    if work is not None:
-                        work.wait()  # side stream waits for this group's gather only
-                    device_decode_mean(self.spec, gathered, stride, self.world, grp.n, x, self.err,
-                                       stream=self.stream, cspec=self.cspec)
+            elif self.world > 1 and self.spec.algorithm != "threshold" and (len(plan) > 1 or plan[0].chunks):
+                # every group (or chunk) is encoded and its allgather started before any
+                # decode: encode(c+1) runs on the SMs while NCCL moves chunk c, decodes
+                # follow in order, each waiting for its own gather only; grids leave
+                # sm_reserve SMs to the NCCL kernels meanwhile
+                lib = _native.lib()
+                prev = lib.mc_set_sm_reserve(self.sm_reserve) if plan[0].chunks else None
+                try:
+                    pending = []
+                    for g, grp in enumerate(plan):
+                        if grp.chunks:
+                            lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
+                            pending += [self._encode_chunk(grp, c, lo | (hi << 64)) for c in grp.chunks]
+                            continue
+                        x = self._encode_group(g, grp)
+                        gathered, stride, work = exchange.allgather_fixed(grp.payload, grp.gather, group=self.pg,
+                                                                          async_op=True)
+                        pending.append((_Chunk(grp.start, grp.end, grp.layout, grp.payload, grp.gather),
+                                        gathered, stride, work))
+                    self._decode_chunks(pending)
+                finally:
+                    if prev is not None:
+                        lib.mc_set_sm_reserve(prev)
             else:
                 for g, grp in enumerate(plan):
                     self._sync_group(g, grp)

@@ -45,6 +45,11 @@ def _rank(rank, world, port, kw, q, peer=False):
         sync = GradSync(CompressorSpec(**kw), prof, partition=Partition(prof.n_tensors, (7, 30)), root_seed=3)
         if peer == "dense":  # the uncompressed all_reduce baseline (config 5's comparator)
             sync.use_dense_allreduce()
+        elif peer == "chunked":  # the N > 1 chunk pipeline on tiny groups: ~1-2K-element chunks
+            sync.chunk_elems = 1024
+            if not all(g.chunks for g in sync._plan(sync.partition)[1:]):
+                q.put((rank, "groups were not chunked"))
+                return
         elif peer == "probe":  # the production entry: store-then-readback probe, then push
             if not sync.try_peer_exchange():
                 q.put((rank, "peer probe failed"))
@@ -134,3 +139,13 @@ def test_two_ranks_dense_allreduce_equals_identity_aggregate():
     """Two ranks: all_reduce(SUM) / 2 is bitwise the reference aggregate of identity payloads
     ((0 + a) + b) / f32(2) — commutative for two terms (for >= 3 ranks only a tolerance)."""
     _run_pair(dict(algorithm="identity"), "dense")
+
+
+@pytest.mark.parametrize("kw", [dict(algorithm="efsignsgd"), dict(algorithm="onebit", bucket_size=50),
+                                dict(algorithm="int8"), dict(algorithm="fp16"), dict(algorithm="identity")],
+                         ids=lambda k: k["algorithm"])
+def test_two_ranks_chunk_pipeline_matches_oracle(kw):
+    """The N > 1 chunk pipeline (every group cut into bucket-aligned chunks, each with its own
+    payload, allgather and decode, all encodes issued before the first decode) equals the
+    oracle's whole-group Trainer.step loop bit for bit: per-bucket codecs are chunk-local."""
+    _run_pair(kw, "chunked")
