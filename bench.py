@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--boundaries", default=None, help="comma separated cut list instead of the search")
     ap.add_argument("--search-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--e2e-chunk", type=int, default=1 << 21, help="elements per pipelined H2D/encode/D2H chunk")
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 23,
+                    help="elements per pipelined H2D/encode/D2H chunk (8M: 32 MB copies, measured best once
+                    consecutive steps overlap; scripts/probes/e2e_debug.py)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl", "allreduce_dense"],
                     help="N > 1: fused encode + push over NVLink peer memory (falls back to NCCL if the "
                          "peer mapping fails on any rank), the NCCL allgather, or auto: the push where the "
@@ -453,8 +455,11 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()  # every sync_host stream waits on the current stream, so this precedes all copies
     for _ in range(args.e2e_steps):
-        sync.sync_host(host_grads, out_host, chunk_elems=args.e2e_chunk)
-    e1.record()  # sync_host leaves the current stream waiting on its D2H and encode streams
+        # each step copies its gradient in and its result out; consecutive steps overlap chunk
+        # by chunk (step t+1's H2D of a chunk waits for step t's read-out of it)
+        sync.sync_host(host_grads, out_host, chunk_elems=args.e2e_chunk, wait=False)
+    sync.sync_host_wait()
+    e1.record()  # the current stream now waits on every step's D2H and encode
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:

@@ -208,8 +208,12 @@ int mc_peer_probe(uint32_t* const* dsts, int32_t n, uint32_t value, void* stream
  * d2h) so PCIe runs full duplex; chunk c of a call waits for the previous call's read-out
  * of the same device chunk.  Chunk-wise encode for identity / fp16 / efsignsgd / onebit /
  * int8, whole-group encode between the chunked copies otherwise.  mc_pipe_finish makes
- * `s_wait` wait for the whole call.  The pipe owns only CUDA events (no device memory). */
+ * `s_wait` wait for the whole call; with s_wait = MC_PIPE_NO_WAIT the call keeps running
+ * and the next call overlaps it (chunk-wise), until a later mc_pipe_finish with a stream
+ * joins them.
+ * The pipe owns only CUDA events (no device memory). */
 typedef struct mc_pipe mc_pipe;
+#define MC_PIPE_NO_WAIT ((void*)(intptr_t)-1)
 int mc_pipe_create(mc_pipe** out);
 void mc_pipe_destroy(mc_pipe* pipe);
 int mc_pipe_group(mc_pipe* pipe, const mc_spec* spec, const float* host_in, float* host_out, float* dev,

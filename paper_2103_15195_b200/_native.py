@@ -23,6 +23,7 @@ MC_ERR_INDEX_RANGE = 0x2
 MC_ERR_INDEX_ORDER = 0x4
 MC_ERR_HEADER = 0x8
 MC_ERR_PEER_TIMEOUT = 0x10
+MC_PIPE_NO_WAIT = ctypes.c_void_p(-1 & 0xFFFFFFFFFFFFFFFF)  # include/mergecomp.h: (void*)(intptr_t)-1
 
 
 class McLayout(ctypes.Structure):

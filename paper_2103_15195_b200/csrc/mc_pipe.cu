@@ -167,7 +167,10 @@ int mc_pipe_group(mc_pipe* p, const mc_spec* s, const float* host_in, float* hos
 
 // End of one host sync: `s_wait` (the caller's stream) waits for every encode and read-out
 // of the call; events of this call are recycled (an event may be re-recorded once all work
-// that waits on it has been enqueued, which is the case here).
+// that waits on it has been enqueued, which is the case here).  s_wait = MC_PIPE_NO_WAIT
+// leaves the call running: the next mc_pipe_group call overlaps it (its H2D of chunk c waits
+// for this call's read-out of chunk c only) — a later mc_pipe_finish with a stream joins
+// both.  (NULL is the legacy default stream, a valid s_wait.)
 int mc_pipe_finish(mc_pipe* p, void* s_enc, void* s_d2h, void* s_wait) {
   if (!p) { set_error("null pipe"); return MC_EINVAL; }
   cudaStream_t se = static_cast<cudaStream_t>(s_enc), sd = static_cast<cudaStream_t>(s_d2h),
@@ -176,9 +179,11 @@ int mc_pipe_finish(mc_pipe* p, void* s_enc, void* s_d2h, void* s_wait) {
   if (!p->out_done) MC_API_CHECK(cudaEventCreateWithFlags(&p->out_done, cudaEventDisableTiming));
   MC_API_CHECK(cudaEventRecord(p->enc_done, se));
   MC_API_CHECK(cudaEventRecord(p->out_done, sd));
-  MC_API_CHECK(cudaStreamWaitEvent(sw, p->enc_done, 0));
-  MC_API_CHECK(cudaStreamWaitEvent(sw, p->out_done, 0));
-  MC_API_CHECK(cudaStreamWaitEvent(se, p->out_done, 0));  // later device steps must not overwrite dev early
+  if (s_wait != MC_PIPE_NO_WAIT) {
+    MC_API_CHECK(cudaStreamWaitEvent(sw, p->enc_done, 0));
+    MC_API_CHECK(cudaStreamWaitEvent(sw, p->out_done, 0));
+    MC_API_CHECK(cudaStreamWaitEvent(se, p->out_done, 0));  // later device steps must not overwrite dev early
+  }
   for (cudaEvent_t e : p->live) p->pool.push_back(e);
   p->live.clear();
   return MC_OK;

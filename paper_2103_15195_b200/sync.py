@@ -300,6 +300,7 @@ class GradSync:
             raise ValueError(f"capture_graph: {self.spec.algorithm} draws per-iteration Philox keys")
         from .compressors import _WS
 
+        self.sync_host_wait()
         part = self.partition if partition is None else self._resolve(partition)
         self.partition = part
         plan = self._plan(part)
@@ -502,6 +503,7 @@ class GradSync:
         group's encode is followed by an asynchronous allgather, and the decodes wait on
         their own gather only — encode(g+1) runs while allgather(g) is on NVLink (the
         compute and communication channels of MergeComp, simulator.py:114-142)."""
+        self.sync_host_wait()
         part = self.partition if partition is None else self._resolve(partition)
         graph = getattr(self, "_graph", None)
         if graph is not None and graph[0] == part.boundaries:
@@ -562,16 +564,20 @@ class GradSync:
         return x
 
     def sync_host(self, host_in: torch.Tensor, host_out: Optional[torch.Tensor] = None,
-                  chunk_elems: int = 1 << 21) -> torch.Tensor:
+                  chunk_elems: int = 1 << 21, wait: bool = True) -> torch.Tensor:
         """The host-buffer entry point: copy a (pinned) host gradient buffer in, run one
         sync step, copy the averaged gradients back out — all stream-ordered.  On one
         rank the whole step is enqueued natively (mc_pipe_group): chunked H2D / fused
-        encode+aggregate / D2H on three streams, PCIe full duplex, and consecutive calls
-        overlap (a chunk is overwritten only after its previous read-out)."""
+        encode+aggregate / D2H on three streams, PCIe full duplex.  ``wait=False`` leaves
+        the step in flight so the next call overlaps it chunk by chunk (its H2D of a chunk
+        waits only for this call's read-out of that chunk): the PCIe fill and drain of
+        consecutive steps coincide.  ``sync_host_wait()`` (or any other step) joins them
+        into the current stream; host_out is complete after that."""
         if host_out is None:
             host_out = torch.empty(self.flat.numel(), dtype=torch.float32, pin_memory=True)
         if self.world == 1 and self.fuse_local and chunk_elems > 0:
-            return self._sync_host_native(host_in, host_out, chunk_elems)
+            return self._sync_host_native(host_in, host_out, chunk_elems, wait)
+        self.sync_host_wait()
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
             self.flat.copy_(host_in, non_blocking=True)
@@ -581,7 +587,17 @@ class GradSync:
         torch.cuda.current_stream(self.device).wait_stream(self.stream)  # host_out is ready in stream order
         return host_out
 
-    def _sync_host_native(self, host_in, host_out, chunk_elems):
+    def sync_host_wait(self) -> None:
+        """Make the current stream wait for every sync_host(wait=False) step in flight."""
+        if getattr(self, "_pipe_pending", False):
+            from .compressors import _stream_ptr
+
+            _native.check(_native.lib().mc_pipe_finish(self._pipe, _stream_ptr(self.stream), _stream_ptr(self._d2h),
+                                                       _stream_ptr(torch.cuda.current_stream(self.device))),
+                          "mc_pipe_finish")
+            self._pipe_pending = False
+
+    def _sync_host_native(self, host_in, host_out, chunk_elems, wait=True):
         import ctypes
 
         from .compressors import _WS, _stream_ptr
@@ -609,7 +625,9 @@ class GradSync:
                 None if grp.residual is None else grp.residual.data_ptr(),
                 None if grp.momentum is None else grp.momentum.data_ptr(), lo, hi, grp.payload.data_ptr(),
                 ws.data_ptr(), ws.numel(), self.err.data_ptr(), sh, se, sd), "mc_pipe_group")
-        _native.check(lib.mc_pipe_finish(self._pipe, se, sd, _stream_ptr(cur)), "mc_pipe_finish")
+        _native.check(lib.mc_pipe_finish(self._pipe, se, sd, _stream_ptr(cur) if wait else _native.MC_PIPE_NO_WAIT),
+                      "mc_pipe_finish")
+        self._pipe_pending = not wait
         self.iteration += 1
         return host_out
 
@@ -648,6 +666,7 @@ class GradSync:
 
     def begin_backward(self) -> None:
         """Arm the hooks for one backward pass under the pinned partition."""
+        self.sync_host_wait()
         plan = self._plan(self.partition)
         ranges = self.partition.group_ranges()
         self._group_of = [g for g, (a, b) in enumerate(ranges) for _ in range(a, b)]
@@ -699,6 +718,7 @@ class GradSync:
         EF residual / momentum.  Rather than carry NaN forever, the state of every cached
         partition is reset to zeros (the codec memory at t = 0) before raising — a skipped
         (e.g. AMP overflow) step costs the EF memory, not the run."""
+        self.sync_host_wait()
         flags = int(self.err.item())
         if flags:
             self.err.zero_()

@@ -182,11 +182,13 @@ def test_backward_overlap_hooks_equal_post_backward_step(algo):
     s1.detach()
 
 
-@pytest.mark.parametrize("algo", ["efsignsgd", "dgc_lite"])
-def test_sync_host_back_to_back_calls(algo):
+@pytest.mark.parametrize("wait", [True, False], ids=["joined", "overlapped"])
+@pytest.mark.parametrize("algo", ["efsignsgd", "dgc_lite", "qsgd"])
+def test_sync_host_back_to_back_calls(algo, wait):
     """Consecutive native host syncs enqueued without a host synchronisation in between
-    (each call's H2D chases the previous call's read-out chunk by chunk) give the same
-    outputs as synchronised device steps."""
+    (each call's H2D chases the previous call's read-out chunk by chunk; overlapped: no call
+    joins the current stream until sync_host_wait) give the same outputs as synchronised
+    device steps."""
     from paper_2103_15195_b200 import gradsets
     from paper_2103_15195_b200.spec import CompressorSpec
     from paper_2103_15195_b200.sync import GradSync
@@ -198,7 +200,8 @@ def test_sync_host_back_to_back_calls(algo):
     ins = [torch.from_numpy(gradsets.synthetic_gradients("resnet50_161", it, 0)).pin_memory() for it in range(3)]
     outs = [torch.empty_like(x).pin_memory() for x in ins]
     for x, o in zip(ins, outs):
-        a.sync_host(x, o, chunk_elems=1 << 19)
+        a.sync_host(x, o, chunk_elems=1 << 19, wait=wait)
+    a.sync_host_wait()
     torch.cuda.synchronize()
     for x, o in zip(ins, outs):
         b.flat.copy_(x)
