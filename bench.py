@@ -43,8 +43,8 @@ def parse():
     ap.add_argument("--search-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 23,
-                    help="elements per pipelined H2D/encode/D2H chunk (8M: 32 MB copies, measured best once
-                    consecutive steps overlap; scripts/probes/e2e_debug.py)")
+                    help="elements per pipelined H2D/encode/D2H chunk (8M: 32 MB copies, measured best once "
+                         "consecutive steps overlap; scripts/probes/e2e_debug.py)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl", "allreduce_dense"],
                     help="N > 1: fused encode + push over NVLink peer memory (falls back to NCCL if the "
                          "peer mapping fails on any rank), the NCCL allgather, or auto: the push where the "
