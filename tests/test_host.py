@@ -204,3 +204,15 @@ def test_package_root_reexports_reference_names():
                  "SearchResult"):
         assert getattr(P, name).__name__ == name
         assert name in P.__all__
+
+
+def test_bench_cli_parses():
+    """bench.py (the driver's entry) parses and prints its usage without a GPU."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--help"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "--e2e-chunk" in r.stdout
