@@ -5,10 +5,8 @@
 // Reference: _compress compressors.py:272-289, randk :278-285, EF :409-413, decode
 // :439-448, aggregate :519-532.  Tie contract for top-k: among
 // equal |x| at the k-th boundary the LOWEST indices are kept.
+#include <algorithm>
 #include <cmath>
-#include <map>
-#include <mutex>
-#include <tuple>
 #include <vector>
 
 #include "mc_internal.cuh"
@@ -972,22 +970,31 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, cons
   // [candidate][warp] mask matrix
   const int64_t s0 = pos - L;
   const uint32_t ex0 = excl_of(p, s0);
-  uint32_t left = w32 * ex0, ex = ex0;
+  const int nc = dwin + RX;
+  uint32_t left = w32 * ex0;
   const uint32_t dl = p.tail_shuffle ? w32 : (0u - w32);
-  const uint32_t de = p.tail_shuffle ? 1u : 0xffffffffu;
-  // hits are queued per thread and tested after the scan, all lanes together: testing them
-  // inside the scan made every warp run the exact test (an integer modulo) whenever any of
-  // its 32 lanes hit (~17% of candidates), not ~0.6%
+  // the filter compares against the largest excl of the range (a superset of the exact
+  // "left < excl_c"; the range moves excl by < 2^11 of ~2^25): branch-free, 32 candidates
+  // per mask word, only the (rare) set bits are queued.  Hits are tested after the scan, all
+  // lanes together: testing them inside the scan made every warp run the exact test (an
+  // integer modulo) whenever any of its 32 lanes hit, not ~0.6% of the time
+  const uint32_t exb = p.tail_shuffle ? ex0 + (uint32_t)nc : ex0;
   uint16_t* q = hitq + tid * HQ;
   int nh = 0;
-#pragma unroll 8
-  for (int c = 0; c < dwin + RX; ++c) {
-    if (left < ex) {
+  for (int c0 = 0; c0 < nc; c0 += 32) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      m |= left < exb ? (1u << j) : 0u;
+      left += dl;
+    }
+    if (nc - c0 < 32) m &= (1u << (nc - c0)) - 1u;
+    while (m) {
+      const int c = c0 + __ffs(m) - 1;
+      m &= m - 1;
       if (nh < HQ) q[nh++] = (uint16_t)c;
       else if (rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);  // (never in practice)
     }
-    left += dl;
-    ex += de;
   }
   const int nmax = __reduce_max_sync(FULL, nh);
   for (int i = 0; i < nmax; ++i) {
@@ -1231,9 +1238,106 @@ __global__ void k_bitmap_all(RP p) {
   }
 }
 
-// ordered compaction of the bitmap -> ascending indices; gather values; EF fix-up
+// Ordered compaction of the bitmap -> ascending indices and values, fused with one
+// streaming pass over the CTA's 32768 elements that is also the encode prologue
+// (compressors.py:381-413): non-finite check, momentum update, EF residual r = c - decode
+// (c where not selected) and, for the fused single-rank sync, out = 0 + decode.  The draw
+// walk never reads the gradient, so it is read once, here.  The CTA publishes its count for
+// the look-back first, streams, stages its selected (offset, value) pairs in shared memory
+// and resolves its output position only at the end — by then every predecessor has
+// published, so nobody waits; the pairs then go out as coalesced rows.  A CTA selecting more
+// than RK_STAGE elements (dense randk) resolves first and writes them from the bitmap before
+// streaming (its values must be read before the pass overwrites the state).
+constexpr int RK_STAGE = 4096;
+template <bool EF, bool MOM, bool VEC>
+__device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uint32_t* s_words, const uint32_t* s_rank,
+                                          uint16_t* s_off, float* s_val, bool stage, bool& bad) {
+  const Prologue& pro = p.pro;
+  for (int i = threadIdx.x; i < TB * 4 * 8; i += blockDim.x) {  // float4 groups, coalesced
+    const int64_t e = e_base + 4 * (int64_t)i;
+    if (e >= p.n) break;
+    const uint32_t wd = s_words[i >> 3];
+    const int sh = (i & 7) * 4;
+    const uint32_t sel4 = (wd >> sh) & 0xfu;
+    uint32_t rk = stage ? s_rank[i >> 3] + __popc(wd & ((1u << sh) - 1u)) : 0u;
+    const bool full = VEC && e + 3 < p.n;
+    float w[4];
+    if (full) {
+      const float4 gv = __ldcs(reinterpret_cast<const float4*>(pro.g + e));
+      w[0] = gv.x; w[1] = gv.y; w[2] = gv.z; w[3] = gv.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = e + q < p.n ? pro.g[e + q] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bad |= !isfinite(w[q]);
+    if (MOM) {
+      float mo[4];
+      if (full) {
+        const float4 mv = *reinterpret_cast<const float4*>(pro.m + e);
+        mo[0] = mv.x; mo[1] = mv.y; mo[2] = mv.z; mo[3] = mv.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mo[q] = e + q < p.n ? pro.m[e + q] : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = pro.signum ? __fadd_rn(__fmul_rn(pro.beta, mo[q]), __fmul_rn(pro.omb, w[q]))
+                          : __fadd_rn(__fmul_rn(pro.beta, mo[q]), w[q]);
+      if (full) *reinterpret_cast<float4*>(pro.m + e) = make_float4(w[0], w[1], w[2], w[3]);
+      else
+        for (int q = 0; q < 4 && e + q < p.n; ++q) pro.m[e + q] = w[q];
+    }
+    double rv[4] = {0.0, 0.0, 0.0, 0.0}, rn[4];
+    if (EF) {
+      if (full) {
+        const double2 r0 = *reinterpret_cast<const double2*>(pro.r + e);
+        const double2 r1 = *reinterpret_cast<const double2*>(pro.r + e + 2);
+        rv[0] = r0.x; rv[1] = r0.y; rv[2] = r1.x; rv[3] = r1.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rv[q] = e + q < p.n ? pro.r[e + q] : 0.0;
+      }
+    }
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double c = EF ? __dadd_rn((double)w[q], rv[q]) : (double)w[q];
+      const float c32 = EF ? __double2float_rn(c) : w[q];
+      const bool sel = (sel4 >> q) & 1u;
+      const float v = p.unbiased ? __fmul_rn(c32, p.scale) : c32;
+      if (EF) rn[q] = sel ? __dsub_rn(c, (double)v) : c;
+      o[q] = sel ? __fadd_rn(0.0f, v) : 0.0f;
+      if (stage && sel) {
+        s_off[rk] = (uint16_t)(4 * i + q);
+        s_val[rk] = v;
+        ++rk;
+      }
+    }
+    if (EF) {
+      if (full) {
+        *reinterpret_cast<double2*>(pro.r + e) = make_double2(rn[0], rn[1]);
+        *reinterpret_cast<double2*>(pro.r + e + 2) = make_double2(rn[2], rn[3]);
+      } else {
+        for (int q = 0; q < 4 && e + q < p.n; ++q) pro.r[e + q] = rn[q];
+      }
+    }
+    if (p.out) {
+      if (full) *reinterpret_cast<float4*>(p.out + e) = make_float4(o[0], o[1], o[2], o[3]);
+      else
+        for (int q = 0; q < 4 && e + q < p.n; ++q) p.out[e + q] = o[q];
+    }
+  }
+}
+
+template <bool EF, bool MOM, bool VEC>
 __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
+  __shared__ uint32_t s_words[TB * 4], s_rank[TB * 4];
+  __shared__ uint16_t s_off[RK_STAGE];
+  __shared__ float s_val[RK_STAGE];
+  __shared__ uint64_t s_pre;
   const int64_t bid = take_ticket(p.w.ticket);
+  if (bid == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   const int64_t nw = cdiv(p.n, 32);
   const int64_t w0 = bid * TB * 4 + (int64_t)threadIdx.x * 4;  // 4 words (128 elements) per thread
   uint32_t words[4];
@@ -1245,99 +1349,53 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
   }
   uint64_t total;
   const uint64_t ex = block_exscan(cnt, &total);
-  const uint64_t pre = block_lookback(p.w.status, bid, total);
-  uint64_t pos = pre + ex;
-  const uint64_t pos_start = pos;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t m = words[q];
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int64_t e = (w0 + q) * 32 + b;
-      float c32;
-      double c;
-      if (p.pro.r) {
-        c = p.pro.r[e];  // pass 1 stored r <- c
-        c32 = __double2float_rn(c);
-      } else {
-        c32 = p.pro.m ? p.pro.m[e] : p.pro.g[e];
-        c = (double)c32;
-      }
-      const float v = p.unbiased ? __fmul_rn(c32, p.scale) : c32;
-      p.idx_out[pos] = (uint32_t)e;
-      p.val_out[pos] = v;
-      if (p.pro.r) p.pro.r[e] = __dsub_rn(c, (double)v);
-      ++pos;
-    }
-  }
-  if (p.out) {  // fused single-rank decode of the CTA's 32768 elements: 0 + v where selected, else 0
-    __shared__ uint32_t s_words[TB * 4], s_rank[TB * 4];
-    uint32_t rk = (uint32_t)pos_start;
+  {
+    uint32_t rk = (uint32_t)ex;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       s_words[threadIdx.x * 4 + q] = words[q];
       s_rank[threadIdx.x * 4 + q] = rk;
       rk += __popc(words[q]);
     }
-    __syncthreads();  // also orders this CTA's val_out writes before the reads below
-    const int64_t e_base = bid * TB * 4 * 32;
-    const bool vec = ((uintptr_t)(p.out + e_base) % 16) == 0;
-    for (int i = threadIdx.x; i < TB * 4 * 8; i += blockDim.x) {  // float4 groups, coalesced
-      const int wi = i >> 3, sh = (i & 7) * 4;
-      const int64_t e = e_base + 4 * (int64_t)i;
-      if (e >= p.n) break;
-      const uint32_t wd = s_words[wi];
-      float v[4];
-      uint32_t r = s_rank[wi] + __popc(wd & ((1u << sh) - 1u));
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool sel = (wd >> (sh + q)) & 1u;
-        v[q] = sel ? __fadd_rn(0.0f, p.val_out[r]) : 0.0f;
-        r += sel;
-      }
-      if (vec && e + 3 < p.n) {
-        *reinterpret_cast<float4*>(p.out + e) = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
-        for (int q = 0; q < 4 && e + q < p.n; ++q) p.out[e + q] = v[q];
-      }
-    }
   }
-}
-
-// prologue pass for randk (momentum/EF state update, non-finite check; no keys needed)
-__global__ void k_sparse_prologue(Prologue pro, int64_t n, uint32_t* err, uint8_t* payload, mc_payload_header hdr,
-                                  float* out) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(payload) = hdr;
+  const int64_t e_base = bid * TB * 4 * 32;
+  const bool stage = total <= RK_STAGE;
   bool bad = false;
-  if (!pro.r && !pro.m && (uintptr_t)pro.g % 16 == 0) {  // only the finiteness check: a pure read
-    constexpr int U = 4;                                    // float4 groups per thread in flight
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x, groups = n / 4;
-    int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    float acc = 0.0f;  // x * 0 + acc stays 0 unless some x is inf / nan
-    for (; gi + (U - 1) * stride < groups; gi += U * stride) {
-      float4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(pro.g) + gi + u * stride);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        acc = __fmaf_rn(v[u].x, 0.0f, __fmaf_rn(v[u].y, 0.0f, __fmaf_rn(v[u].z, 0.0f, __fmaf_rn(v[u].w, 0.0f, acc))));
+  if (stage) {
+    if (threadIdx.x == 0) st_volatile(&p.w.status[bid], (bid == 0 ? LB_PRE : LB_AGG) | total);  // early
+    __syncthreads();
+    rk_stream<EF, MOM, VEC>(p, e_base, s_words, s_rank, s_off, s_val, true, bad);
+    if ((threadIdx.x >> 5) == 0) {
+      const uint64_t pre = lookback_warp(p.w.status, bid, total);
+      if (threadIdx.x == 0) s_pre = pre;
     }
-    for (; gi < groups; gi += stride) {
-      const float4 v = reinterpret_cast<const float4*>(pro.g)[gi];
-      acc = __fmaf_rn(v.x, 0.0f, __fmaf_rn(v.y, 0.0f, __fmaf_rn(v.z, 0.0f, __fmaf_rn(v.w, 0.0f, acc))));
+    __syncthreads();
+    const uint64_t pre = s_pre;
+    for (int j = threadIdx.x; j < (int)total; j += blockDim.x) {
+      p.idx_out[pre + j] = (uint32_t)(e_base + s_off[j]);
+      p.val_out[pre + j] = s_val[j];
     }
-    for (int64_t e = 4 * groups + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride)
-      acc = __fmaf_rn(pro.g[e], 0.0f, acc);
-    bad = acc != 0.0f;
   } else {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-      float c32;
-      const double c = pro.load(e, c32, bad, true);
-      if (pro.r) pro.r[e] = c;
+    const uint64_t pre = block_lookback(p.w.status, bid, total);
+    uint64_t pos = pre + ex;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t m = words[q];
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t e = (w0 + q) * 32 + b;
+        float c32;
+        p.pro.load(e, c32, bad, false);  // the state is written by the streaming pass below
+        p.idx_out[pos] = (uint32_t)e;
+        p.val_out[pos] = p.unbiased ? __fmul_rn(c32, p.scale) : c32;
+        ++pos;
+      }
     }
+    __syncthreads();  // every selected value was read before the pass overwrites the state
+    rk_stream<EF, MOM, VEC>(p, e_base, s_words, s_rank, s_off, s_val, false, bad);
   }
-  flag(err, bad, MC_ERR_NONFINITE);
+  flag(p.err, bad, MC_ERR_NONFINITE);
 }
 
 // ------------------------------------------------------------------ sparse decode-mean
@@ -1535,33 +1593,54 @@ int encode_threshold(const EncodeArgs& a, float* out) {
 struct RandkStats {
   double sd, window_mean_max;
 };
-// Lemire rejection probability of step s is ((2^32 - excl) mod excl) / 2^32 (a sawtooth in
-// excl); summed over the k steps it gives the variance of the walk's drift, and its
-// 1024-step sliding sums the per-window means.  O(k) on the host, cached per group shape.
+// Lemire rejection probability of step s is ((2^32 - excl) mod excl) / 2^32 = 1 - q excl / 2^32
+// with q = floor(2^32 / excl): linear in excl on every run of equal q (a sawtooth).  The k
+// steps cover excl in [lo, lo + k), so the sums over each run are closed forms — the variance
+// of the walk's drift and the largest mean rejection count of a 1024-step window (piecewise
+// linear in the window start: maximal where a window starts or ends at a run boundary) in
+// O(number of runs), no per-step loop and no cache.
 RandkStats randk_stats(int64_t n, int64_t k, bool tail_shuffle) {
-  static std::mutex mu;
-  static std::map<std::tuple<int64_t, int64_t, bool>, RandkStats> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_tuple(n, k, tail_shuffle);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  std::vector<double> pr((size_t)k);
-  double var = 0.0;
-  for (int64_t st = 0; st < k; ++st) {
-    const uint64_t ex = tail_shuffle ? (uint64_t)(n - st) : (uint64_t)(n - k + 1 + st);
-    const double pv = (double)((0x100000000ull - ex) % ex) / 4294967296.0;
-    pr[(size_t)st] = pv;
-    var += pv * (1.0 - pv);
+  const long double T = 4294967296.0L;
+  (void)tail_shuffle;  // Floyd walks excl = n-k+1 .. n upwards, the tail shuffle n .. n-k+1 down:
+  const int64_t lo = n - k + 1, hi = n;  // the same values, and the same set of 1024-step windows
+  auto q_of = [](int64_t e) { return (int64_t)(0x100000000ll / e); };
+  // sum of p over excl in [a, b] (one run of constant q), and of p^2
+  auto run_sums = [&](int64_t a, int64_t b, int64_t q, long double& s1, long double& s2) {
+    const long double m = (long double)(b - a + 1), se = ((long double)a + b) * m / 2.0L;
+    auto sq = [](long double x) { return x * (x + 1) * (2 * x + 1) / 6.0L; };
+    const long double se2 = sq((long double)b) - sq((long double)a - 1);
+    s1 = (m * T - q * se) / T;
+    s2 = (m * T * T - 2.0L * T * q * se + (long double)q * q * se2) / (T * T);
+  };
+  std::vector<int64_t> bnd;  // run starts in [lo, hi]
+  long double var = 0.0L;
+  for (int64_t a = lo; a <= hi;) {
+    const int64_t q = q_of(a), b = imin(hi, 0x100000000ll / q);  // last excl with the same q
+    long double s1, s2;
+    run_sums(a, b, q, s1, s2);
+    var += s1 - s2;
+    bnd.push_back(a);
+    a = b + 1;
   }
-  double win = 0.0, best = 0.0;
-  for (int64_t st = 0; st < k; ++st) {
-    win += pr[(size_t)st];
-    if (st >= WP) win -= pr[(size_t)(st - WP)];
-    best = win > best ? win : best;
-  }
-  const RandkStats r{sqrt(var), best};
-  cache.emplace(key, r);
-  return r;
+  // window sum over excl [x, x + W) via runs
+  auto wsum = [&](int64_t x) {
+    const int64_t y = imin(hi, x + WP - 1);
+    long double t = 0.0L;
+    for (int64_t a = x; a <= y;) {
+      const int64_t q = q_of(a), b = imin(y, 0x100000000ll / q);
+      long double s1, s2;
+      run_sums(a, b, q, s1, s2);
+      t += s1;
+      a = b + 1;
+    }
+    return (double)t;
+  };
+  // breakpoints of the window start x: x or x + WP - 1 on a run boundary
+  double best = std::max(wsum(lo), wsum(imax(lo, hi - WP + 1)));
+  for (int64_t r : bnd)
+    for (int64_t x : {r, r - WP, r - WP + 1})
+      if (x >= lo && x <= hi) best = std::max(best, wsum(x));
+  return RandkStats{sqrt((double)var), best};
 }
 
 int encode_randk(const EncodeArgs& a, float* out) {
@@ -1591,8 +1670,6 @@ int encode_randk(const EncodeArgs& a, float* out) {
   MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st));
   MC_API_CHECK(cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st));
   MC_API_CHECK(cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st));
-  const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 256), (int64_t)sm_count() * 4));
-  note_launch(); k_sparse_prologue<<<g1, 256, 0, st>>>(p.pro, n, p.err, p.payload, p.hdr, out);
   if (k == n) {
     note_launch(); k_bitmap_all<<<(unsigned)imax(1, imin(cdiv(nwords, 256), 1024)), 256, 0, st>>>(p);
   } else {
@@ -1655,7 +1732,18 @@ int encode_randk(const EncodeArgs& a, float* out) {
       note_launch(); k_randk_floyd_mark<<<gk, 256, 0, st>>>(p);
     }
   }
-  note_launch(); k_randk_emit<<<(unsigned)cdiv(nwords, TB * 4), TB, 0, st>>>(p);
+  const bool vec = (uintptr_t)p.pro.g % 16 == 0 && (!out || (uintptr_t)out % 16 == 0) &&
+                   (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) && (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0);
+  const unsigned ge = (unsigned)cdiv(nwords, TB * 4);
+  note_launch();
+#define MC_RK_EMIT(EF, MOM)                                                 \
+  if (vec) k_randk_emit<EF, MOM, true><<<ge, TB, 0, st>>>(p);               \
+  else k_randk_emit<EF, MOM, false><<<ge, TB, 0, st>>>(p);
+  if (p.pro.r && p.pro.m) { MC_RK_EMIT(true, true) }
+  else if (p.pro.r) { MC_RK_EMIT(true, false) }
+  else if (p.pro.m) { MC_RK_EMIT(false, true) }
+  else { MC_RK_EMIT(false, false) }
+#undef MC_RK_EMIT
   MC_LAUNCH_CHECK();
   return MC_OK;
 }
