@@ -895,59 +895,54 @@ __device__ __forceinline__ bool rejects(const RP& p, uint32_t w32, int64_t s) {
   return left < ex && left < (0u - ex) % ex;
 }
 
-// per window: expected rejections (expw[w]) and their variance (expw[nwin + w])
-__global__ void k_randk_expect(RP p, double* expw, int64_t nwin) {
-  __shared__ double part[8], vpart[8];
-  const int64_t w = blockIdx.x;
-  double acc = 0.0, var = 0.0;
-  for (int i = threadIdx.x; i < WP; i += blockDim.x) {
-    const int64_t s = imin(imax(w * WP + i, 0), p.k - 1);
-    const uint32_t ex = excl_of(p, s);
-    const double pr = (double)((0u - ex) % ex) * 0x1.0p-32;
-    acc += pr;
-    var += pr * (1.0 - pr);
+// Mean and variance of the rejections before draw-stream position S (steps clamp(s, 0, k-1),
+// as the windows count them): step s rejects with p = r / 2^32, r = 2^32 mod excl(s), and on a
+// run of equal q = floor(2^32 / excl) the remainder falls by q per unit of excl, so the sums
+// over a run are closed forms in (m, r_first, q) — a few runs cover the whole stream.
+__device__ void randk_drift(const RP& p, int64_t S, double& mean, double& var) {
+  const int64_t k = p.k, n = p.n, S1 = S < k ? S : k;
+  mean = var = 0.0;
+  if (S1 > 0) {
+    // excl values of steps [0, S1): ascending n-k+1 .. (Floyd) or the top S1 values (tail shuffle)
+    int64_t a = p.tail_shuffle ? n - S1 + 1 : n - k + 1;
+    const int64_t b = p.tail_shuffle ? n : n - k + S1;
+    const double T = 4294967296.0;
+    while (a <= b) {
+      const int64_t q = 0x100000000ll / a, e = imin(b, 0x100000000ll / q);
+      const double m = (double)(e - a + 1), r0 = (double)(0x100000000ll - q * a), qd = (double)q;
+      const double sj = m * (m - 1.0) / 2.0, sj2 = (m - 1.0) * m * (2.0 * m - 1.0) / 6.0;
+      const double s1 = (m * r0 - qd * sj) / T;                                   // sum p
+      const double s2 = (m * r0 * r0 - 2.0 * r0 * qd * sj + qd * qd * sj2) / (T * T);  // sum p^2
+      mean += s1;
+      var += s1 - s2;
+      a = e + 1;
+    }
   }
-  for (int o = 16; o; o >>= 1) {
-    acc += __shfl_xor_sync(FULL, acc, o);
-    var += __shfl_xor_sync(FULL, var, o);
-  }
-  if ((threadIdx.x & 31) == 0) { part[threadIdx.x >> 5] = acc; vpart[threadIdx.x >> 5] = var; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0, v = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { t += part[i]; v += vpart[i]; }
-    expw[w] = t;
-    expw[nwin + w] = v;
+  if (S > k) {  // positions past the last step count it again
+    const uint32_t ex = excl_of(p, k - 1);
+    const double pl = (double)((0u - ex) % ex) * 0x1.0p-32;
+    mean += (double)(S - k) * pl;
+    var += (double)(S - k) * pl * (1.0 - pl);
   }
 }
 
 constexpr int HQ = 16;  // queued filter hits per thread (mean ~3.2 at 1% density)
 template <int DW, int RX>
-__global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, const double* expw, int64_t nwin,
-                               int64_t* Lw, uint8_t* tables) {
+__global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int64_t nwin, int64_t* Lw,
+                               uint8_t* tables) {
   extern __shared__ uint32_t masks[];  // [DW + RX][32] then the hit queues [1024][HQ] u16
   uint16_t* hitq = reinterpret_cast<uint16_t*>(masks + (DW + RX) * 32);
   __shared__ int64_t s_L;
   __shared__ int s_dw;
-  __shared__ double s_part[32], s_vpart[32];
   const int64_t w = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {  // expected offset at the window start and its variance: sums over the earlier windows
-     // (block reduction; they only centre and size the speculated range — the chain checks it).
-     // The range is +-(7 sd + 16), at most DW: early windows, whose offset is still nearly
-     // deterministic, evaluate a few dozen entering offsets instead of DW
-    double e = 0.0, v = 0.0;
-    for (int64_t i = tid; i < w; i += blockDim.x) { e += expw[i]; v += expw[nwin + i]; }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      e += __shfl_xor_sync(FULL, e, o);
-      v += __shfl_xor_sync(FULL, v, o);
-    }
-    if (lane == 0) { s_part[warp] = e; s_vpart[warp] = v; }
-    __syncthreads();
+  {  // expected offset at the window start and its variance (closed form; they only centre
+     // and size the speculated range — the chain checks it).  The range is +-(7 sd + 16), at
+     // most DW: early windows, whose offset is still nearly deterministic, evaluate a few
+     // dozen entering offsets instead of DW
     if (tid == 0) {
-      double t = 0.0, vv = 0.0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { t += s_part[i]; vv += s_vpart[i]; }
+      double t, vv;
+      randk_drift(p, w * WP, t, vv);
       const int half = (int)ceil(7.0 * sqrt(vv)) + 16;
       const int dw = (int)imin(DW, (int64_t)((2 * half + 31) / 32 * 32));
       const int64_t L = imax(0, (int64_t)floor(t) - dw / 2);
@@ -1678,7 +1673,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
     const int64_t nwords = imin(n, k + k / 16 + 4096);
     const int64_t nwin = cdiv(nwords, WP);
     uint8_t* wsb = reinterpret_cast<uint8_t*>(p.w.list) + a16(4 * nwords);
-    double* expw = reinterpret_cast<double*>(wsb);  // [2][nwin]: expectation, variance
+    // wsb[0, 16 nwin): spare (the per-window drift sums are closed forms now, randk_drift)
     int64_t* Lw = reinterpret_cast<int64_t*>(wsb + a16(16 * nwin));
     int64_t* tin = reinterpret_cast<int64_t*>(wsb + a16(16 * nwin) + a16(8 * nwin));
     WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + a16(16 * nwin) + 2 * a16(8 * nwin));
@@ -1702,13 +1697,12 @@ int encode_randk(const EncodeArgs& a, float* out) {
     if (4 * n >= a16(4 * nwords) + a16(16 * nwin) + 2 * a16(8 * nwin) + 64 + a16(nwin * DWr) +
                      4 * (cdiv(nwin, CG) * (DWr + 1) + 4 + nwin * DWr)) {  // room for the parallel walk
       const int64_t ngrp = cdiv(nwin, CG);
-      note_launch(); k_randk_expect<<<(unsigned)nwin, 256, 0, st>>>(p, expw, nwin);
 #define MC_RANDK_WALK(DWV, RXV)                                                                                    \
   {                                                                                                               \
     const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2;                                                          \
     static std::atomic<uint64_t> cfg{0}; /* per device */                                                         \
     MC_API_CHECK(smem_optin(cfg, k_randk_tables<DWV, RXV>, ts));                                                  \
-    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, expw, nwin, Lw, tables); \
+    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, nwin, Lw, tables); \
     note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp, mid);                 \
     note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, mid, tg, tin, ctl);              \
     note_launch(); k_randk_emit_draws<RXV><<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);           \
