@@ -117,6 +117,15 @@ int64_t mc_encode_workspace_bytes(const mc_spec* spec, int64_t n);
 int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t group,
                    uint64_t* key_lo, uint64_t* key_hi);
 
+/* The same keys computed on the device for a CUDA Graph that replays across iterations:
+ * keys[2g], keys[2g+1] = derive_seed(root, worker, *iteration, group0 + g) for g < ngroups,
+ * then *iteration += 1 (iteration: device u64; keys: device u64[2 * ngroups]).  The _dk
+ * encode variants read their Philox key from such a device pair instead of (key_lo, key_hi),
+ * so a captured step draws the right stream on every replay (numpy's per-(worker, iteration,
+ * group) Generator, compressors.py:247-251). */
+int mc_derive_keys(uint64_t root, uint64_t worker, uint64_t* iteration, uint64_t group0, int32_t ngroups,
+                   uint64_t* keys, void* stream);
+
 /* Encode one group of n fp32 gradients into `payload` (device, >= layout.bytes).
  * residual (f64[n]) must be non-null iff spec->error_feedback; momentum (f32[n])
  * iff spec->has_momentum.  Both are updated in place.  (key_lo, key_hi) is the
@@ -131,6 +140,14 @@ int mc_encode(const mc_spec* spec, const float* grad, int64_t n, double* residua
 int mc_encode_decode(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
                      uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
                      float* out, uint32_t* err_flags, void* stream);
+
+/* mc_encode / mc_encode_decode with the Philox key read from device memory (dkey[0..1]). */
+int mc_encode_dk(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+                 const uint64_t* dkey, void* payload, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                 void* stream);
+int mc_encode_decode_dk(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+                        const uint64_t* dkey, void* payload, void* workspace, int64_t workspace_bytes, float* out,
+                        uint32_t* err_flags, void* stream);
 
 /* Chunked variant for pipelining host<->device copies with compute: encode elements
  * [begin, begin+count) of an n-element group whose buffers start at grad / residual /

@@ -215,10 +215,12 @@ def split_seed(seed: int) -> tuple[int, int]:
 
 def device_encode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],
                   momentum: Optional[torch.Tensor], seed: int, out: Optional[torch.Tensor] = None,
-                  err: Optional[torch.Tensor] = None, stream=None, cspec=None) -> DevicePayload:
+                  err: Optional[torch.Tensor] = None, stream=None, cspec=None,
+                  dkey: Optional[torch.Tensor] = None) -> DevicePayload:
     """Enqueue one encode on the current (or given) stream; no host sync.  ``residual``
     (f64) and ``momentum`` (f32) are updated in place.  ``err`` (int32[1]) collects
-    the device error flags."""
+    the device error flags.  ``dkey`` (a device int64[2] written by ``derive_keys``)
+    replaces ``seed`` by a key read on the device (CUDA Graph replays)."""
     n = grad.numel()
     cs = cspec if cspec is not None else spec.to_c()
     L = _native.layout(cs, n)
@@ -228,6 +230,14 @@ def device_encode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[t
     ws = _WS.get(grad.device, wsb, stream)
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=grad.device)
+    if dkey is not None:
+        _native.check(
+            _native.lib().mc_encode_dk(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum),
+                                       dkey.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), err.data_ptr(),
+                                       _stream_ptr(stream)),
+            "mc_encode_dk",
+        )
+        return DevicePayload(spec, n, out, L)
     lo, hi = split_seed(seed)
     _native.check(
         _native.lib().mc_encode(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum), lo, hi,
@@ -240,9 +250,9 @@ def device_encode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[t
 def device_encode_decode(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],
                          momentum: Optional[torch.Tensor], seed: int, out: torch.Tensor,
                          payload: Optional[torch.Tensor] = None, err: Optional[torch.Tensor] = None, stream=None,
-                         cspec=None) -> DevicePayload:
+                         cspec=None, dkey: Optional[torch.Tensor] = None) -> DevicePayload:
     """Single-rank sync in one pass where the codec allows it: encode ``grad`` and write
-    ``out = aggregate([payload])`` (``out`` may alias ``grad``)."""
+    ``out = aggregate([payload])`` (``out`` may alias ``grad``).  ``dkey``: see device_encode."""
     n = grad.numel()
     cs = cspec if cspec is not None else spec.to_c()
     L = _native.layout(cs, n)
@@ -251,6 +261,14 @@ def device_encode_decode(spec: CompressorSpec, grad: torch.Tensor, residual: Opt
     ws = _WS.get(grad.device, _native.workspace_bytes(cs, n), stream)
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=grad.device)
+    if dkey is not None:
+        _native.check(
+            _native.lib().mc_encode_decode_dk(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum),
+                                              dkey.data_ptr(), payload.data_ptr(), ws.data_ptr(), ws.numel(),
+                                              out.data_ptr(), err.data_ptr(), _stream_ptr(stream)),
+            "mc_encode_decode_dk",
+        )
+        return DevicePayload(spec, n, payload, L)
     lo, hi = split_seed(seed)
     _native.check(
         _native.lib().mc_encode_decode(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum), lo, hi,
@@ -259,6 +277,17 @@ def device_encode_decode(spec: CompressorSpec, grad: torch.Tensor, residual: Opt
         "mc_encode_decode",
     )
     return DevicePayload(spec, n, payload, L)
+
+
+def derive_keys(root: int, worker: int, iteration: torch.Tensor, keys: torch.Tensor, group0: int = 0,
+                stream=None) -> None:
+    """keys[g] = derive_seed(root, worker, iteration, group0 + g) for every row of ``keys``
+    (device int64[G, 2]), computed on the device from the device counter ``iteration``
+    (int64[1]), which is then advanced by one (mc_derive_keys): the key schedule of a
+    captured CUDA Graph."""
+    _native.check(_native.lib().mc_derive_keys(int(root), int(worker), iteration.data_ptr(), int(group0),
+                                               keys.shape[0], keys.data_ptr(), _stream_ptr(stream)),
+                  "mc_derive_keys")
 
 
 def device_encode_push(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],

@@ -104,19 +104,62 @@ int fill_layout(const mc_spec* s, int64_t n, int64_t cap, mc_layout* L) {
 namespace seedseq {
 constexpr uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u, INIT_B = 0x8b51f9ddu, MULT_B = 0x58f38dedu;
 constexpr uint32_t MIX_L = 0xca01f9ddu, MIX_R = 0x4973f715u;
-static uint32_t hashmix(uint32_t v, uint32_t& hc) {
+__host__ __device__ inline uint32_t hashmix(uint32_t v, uint32_t& hc) {
   v ^= hc;
   hc *= MULT_A;
   v *= hc;
   v ^= v >> 16;
   return v;
 }
-static uint32_t mix(uint32_t x, uint32_t y) {
+__host__ __device__ inline uint32_t mix(uint32_t x, uint32_t y) {
   uint32_t r = MIX_L * x - MIX_R * y;
   r ^= r >> 16;
   return r;
 }
+// SeedSequence(entropy=(root, worker, iteration, group)).generate_state(2, u64) — the same
+// code on the host (mc_derive_seed) and on the device (mc_derive_keys)
+__host__ __device__ inline void derive(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t group,
+                                       uint64_t& key_lo, uint64_t& key_hi) {
+  uint32_t ent[8];
+  int ne = 0;
+  const uint64_t in[4] = {root, worker, iteration, group};
+  for (int i = 0; i < 4; ++i) {  // _coerce_to_uint32_array: 0 -> [0], else little-endian 32-bit words
+    uint64_t v = in[i];
+    if (v == 0) { ent[ne++] = 0; continue; }
+    while (v) { ent[ne++] = (uint32_t)(v & 0xffffffffu); v >>= 32; }
+  }
+  uint32_t pool[4];
+  uint32_t hc = INIT_A;
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < ne ? ent[i] : 0u, hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s], hc));
+  for (int s = 4; s < ne; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[s], hc));
+  uint32_t st[4];
+  uint32_t hb = INIT_B;
+  for (int i = 0; i < 4; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hb;
+    hb *= MULT_B;
+    v *= hb;
+    v ^= v >> 16;
+    st[i] = v;
+  }
+  key_lo = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+  key_hi = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+}
 }  // namespace seedseq
+
+// keys[g] = derive(root, worker, *iteration, group0 + g); then *iteration += 1 (one CTA)
+__global__ void k_derive_keys(uint64_t root, uint64_t worker, uint64_t* iteration, uint64_t group0, int ngroups,
+                              uint64_t* keys) {
+  const uint64_t it = *iteration;
+  for (int g = threadIdx.x; g < ngroups; g += blockDim.x)
+    seedseq::derive(root, worker, it, group0 + (uint64_t)g, keys[2 * g], keys[2 * g + 1]);
+  __syncthreads();
+  if (threadIdx.x == 0) *iteration = it + 1;
+}
 
 }  // namespace mc
 
@@ -169,36 +212,17 @@ int64_t mc_encode_workspace_bytes(const mc_spec* s, int64_t n) {
 
 int mc_derive_seed(uint64_t root, uint64_t worker, uint64_t iteration, uint64_t group, uint64_t* key_lo,
                    uint64_t* key_hi) {
-  using namespace seedseq;
   if (!key_lo || !key_hi) { set_error("null output"); return MC_EINVAL; }
-  uint32_t ent[8];
-  int ne = 0;
-  const uint64_t in[4] = {root, worker, iteration, group};
-  for (int i = 0; i < 4; ++i) {  // _coerce_to_uint32_array: 0 -> [0], else little-endian 32-bit words
-    uint64_t v = in[i];
-    if (v == 0) { ent[ne++] = 0; continue; }
-    while (v) { ent[ne++] = (uint32_t)(v & 0xffffffffu); v >>= 32; }
-  }
-  uint32_t pool[4];
-  uint32_t hc = INIT_A;
-  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < ne ? ent[i] : 0u, hc);
-  for (int s = 0; s < 4; ++s)
-    for (int d = 0; d < 4; ++d)
-      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s], hc));
-  for (int s = 4; s < ne; ++s)
-    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[s], hc));
-  uint32_t st[4];
-  uint32_t hb = INIT_B;
-  for (int i = 0; i < 4; ++i) {
-    uint32_t v = pool[i % 4];
-    v ^= hb;
-    hb *= MULT_B;
-    v *= hb;
-    v ^= v >> 16;
-    st[i] = v;
-  }
-  *key_lo = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
-  *key_hi = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+  seedseq::derive(root, worker, iteration, group, *key_lo, *key_hi);
+  return MC_OK;
+}
+
+int mc_derive_keys(uint64_t root, uint64_t worker, uint64_t* iteration, uint64_t group0, int32_t ngroups,
+                   uint64_t* keys, void* stream) {
+  if (!iteration || !keys || ngroups < 1) { set_error("bad mc_derive_keys arguments"); return MC_EINVAL; }
+  note_launch();
+  k_derive_keys<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(root, worker, iteration, group0, ngroups, keys);
+  MC_LAUNCH_CHECK();
   return MC_OK;
 }
 
@@ -206,7 +230,7 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
                        uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
                        uint32_t* err_flags, void* stream, float* out, int64_t begin = 0, int64_t count = -1,
                        int npush = 0, void* const* push_dsts = nullptr, uint32_t* const* push_flags = nullptr,
-                       uint32_t epoch = 0) {
+                       uint32_t epoch = 0, const uint64_t* dkey = nullptr) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
   if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
@@ -238,6 +262,7 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
   a.push_dsts = push_dsts;
   a.push_flags = push_flags;
   a.epoch = epoch;
+  a.dkey = dkey;
   if (begin != 0 || (count >= 0 && count != n)) {  // chunked: deterministic elementwise / bucketed codecs only
     const int al = s->algorithm;
     if (begin < 0 || count < 1 || begin + count > n) { set_error("bad chunk [%lld, +%lld)", (long long)begin, (long long)count); return MC_EINVAL; }
@@ -460,6 +485,24 @@ int mc_encode_range(const mc_spec* s, const float* grad, int64_t n, int64_t begi
                              err_flags, stream, out, begin, count);
   if (rc == MC_FUSED_UNSUPPORTED) { set_error("fused decode unavailable on this path"); return MC_EINVAL; }
   return rc;
+}
+
+int mc_encode_dk(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                 const uint64_t* dkey, void* payload, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                 void* stream) {
+  if (!dkey) { set_error("null device key"); return MC_EINVAL; }
+  return encode_impl(s, grad, n, residual, momentum, 0, 0, payload, workspace, workspace_bytes, err_flags, stream,
+                     nullptr, 0, -1, 0, nullptr, nullptr, 0, dkey);
+}
+
+int mc_encode_decode_dk(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                        const uint64_t* dkey, void* payload, void* workspace, int64_t workspace_bytes, float* out,
+                        uint32_t* err_flags, void* stream) {
+  if (!out || !dkey) { set_error("null output or device key"); return MC_EINVAL; }
+  const int rc = encode_impl(s, grad, n, residual, momentum, 0, 0, payload, workspace, workspace_bytes, err_flags,
+                             stream, out, 0, -1, 0, nullptr, nullptr, 0, dkey);
+  if (rc != MC_FUSED_UNSUPPORTED) return rc;
+  return mc_decode_mean_ws(s, payload, 0, 1, n, out, workspace, workspace_bytes, err_flags, stream);
 }
 
 int mc_encode_decode(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,

@@ -103,15 +103,20 @@ struct Philox {
 struct PhiloxKS {
   uint64_t a[10], b[10];
   uint64_t x1, x2;  // hi(M0 a0) ^ b1 and lo(M0 a0) ^ b2: round 1's M0 product is a key constant
-  static PhiloxKS make(uint64_t k0, uint64_t k1) {
+  __host__ __device__ static PhiloxKS make(uint64_t k0, uint64_t k1) {
     PhiloxKS ks;
     for (int r = 0; r < 10; ++r) {
       ks.a[r] = k0 + (uint64_t)r * 0x9E3779B97F4A7C15ull;
       ks.b[r] = k1 + (uint64_t)r * 0xBB67AE8584CAA73Bull;
     }
+#ifdef __CUDA_ARCH__
+    const uint64_t ulo = 0xD2E7470EE14C6C93ull * ks.a[0], uhi = __umul64hi(0xD2E7470EE14C6C93ull, ks.a[0]);
+#else
     const unsigned __int128 u = (unsigned __int128)0xD2E7470EE14C6C93ull * ks.a[0];
-    ks.x1 = (uint64_t)(u >> 64) ^ ks.b[1];
-    ks.x2 = (uint64_t)u ^ ks.b[2];
+    const uint64_t ulo = (uint64_t)u, uhi = (uint64_t)(u >> 64);
+#endif
+    ks.x1 = uhi ^ ks.b[1];
+    ks.x2 = ulo ^ ks.b[2];
     return ks;
   }
   // One block whose counter ctr = blk + 1 fits 32 bits (streams under 2^34 draws).  Round 0
@@ -544,6 +549,9 @@ struct EncodeArgs {
   void* const* push_dsts = nullptr;       // host array [npush] of device pointers
   uint32_t* const* push_flags = nullptr;  // host array [npush] of device pointers
   uint32_t epoch = 0;
+  // graph-capturable keys (mc_encode_dk / mc_encode_decode_dk): the 128-bit Philox key is
+  // read on the device from dkey[0..1] (written by mc_derive_keys) instead of (k0, k1)
+  const uint64_t* dkey = nullptr;
 };
 
 constexpr int MC_MAX_PUSH = 16;

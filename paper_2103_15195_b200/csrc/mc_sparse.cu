@@ -673,7 +673,11 @@ struct RP {
   int tail_shuffle;  // numpy's tail-shuffle branch (k > n//50 and n > 10000)
   uint8_t* payload;
   mc_payload_header hdr;
+  const uint64_t* dkey;  // device-resident Philox key (graph capture) or null: (k0, k1)
 };
+__device__ __forceinline__ Philox randk_philox(const RP& p) {
+  return p.dkey ? Philox{p.dkey[0], p.dkey[1]} : Philox{p.k0, p.k1};
+}
 
 __device__ __forceinline__ uint32_t draw32(const Philox& ph, uint64_t pos) {
   uint64_t w[4];
@@ -698,7 +702,7 @@ __device__ __forceinline__ uint64_t step_range(const RP& p, int64_t s) {
 
 // 32-bit draw stream precomputed in parallel (8 words per Philox block).
 __global__ void k_randk_words(RP p, uint32_t* words, int64_t nwords) {
-  const Philox ph{p.k0, p.k1};
+  const Philox ph = randk_philox(p);
   for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 8 * blk < nwords;
        blk += (int64_t)gridDim.x * blockDim.x) {
     uint64_t w[4];
@@ -728,7 +732,7 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
   __shared__ int s_nw;
   __shared__ int64_t s_base, s_t0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Philox ph{p.k0, p.k1};
+  const Philox ph = randk_philox(p);
   if (start && start[0] < 0) return;  // the multi-SM walk served every step
   if (tid == 0) { s_base = start ? start[0] : 0; s_t0 = start ? start[1] : 0; }
   __syncthreads();
@@ -954,7 +958,7 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int6
   __syncthreads();
   const int64_t L = s_L;
   const int dwin = s_dw;
-  const Philox ph{p.k0, p.k1};
+  const Philox ph = randk_philox(p);
   const int64_t pos = w * WP + tid;
   const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
   for (int i = tid; i < (dwin + RX) * 32; i += blockDim.x) masks[i] = 0u;
@@ -1111,7 +1115,7 @@ __global__ void __launch_bounds__(1024) k_randk_emit_draws(RP p, const uint32_t*
   if (w >= ctl->nwin_used) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t0 = tin[w];
-  const Philox ph{p.k0, p.k1};
+  const Philox ph = randk_philox(p);
   const int64_t pos = w * WP + tid;
   const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
   for (int d = 0; d < RX; ++d) {
@@ -1646,6 +1650,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
   p.k = k;
   p.k0 = a.k0;
   p.k1 = a.k1;
+  p.dkey = a.dkey;
   p.w = carve(a.ws, n, k);
   p.err = a.ctx.err;
   p.idx_out = reinterpret_cast<uint32_t*>(a.payload + a.L.off_idx);

@@ -229,8 +229,9 @@ class GradSync:
         self.flat.copy_(flat, non_blocking=True)
 
     # ------------------------------------------------------------ the sync step
-    def _sync_group(self, g: int, grp: _Group) -> int:
-        """Enqueue encode -> allgather -> decode_mean for one group; returns kernel launches."""
+    def _sync_group(self, g: int, grp: _Group, dkey: Optional[torch.Tensor] = None) -> int:
+        """Enqueue encode -> allgather -> decode_mean for one group; returns kernel launches.
+        ``dkey``: the group's Philox key on the device (graph capture) instead of a host key."""
         seed = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
         x = self.flat[grp.start:grp.end]
         probe = self.probe is not None and self.probe[0] == g
@@ -241,7 +242,7 @@ class GradSync:
         if self.world == 1 and self.fuse_local:
             # single rank: aggregate([payload]) written by the encode pass itself (in place)
             device_encode_decode(self.spec, x, grp.residual, grp.momentum, key, x, payload=grp.payload, err=self.err,
-                                 stream=self.stream, cspec=self.cspec)
+                                 stream=self.stream, cspec=self.cspec, dkey=dkey)
             if probe:
                 ev[1].record(self.stream)
                 self.probe[1].append(ev)
@@ -284,21 +285,20 @@ class GradSync:
                                stream=self.stream, cspec=self.cspec)
 
     # ------------------------------------------------------------ CUDA Graph of a pinned partition
-    GRAPHABLE = frozenset({"identity", "fp16", "efsignsgd", "onebit", "int8", "signsgd", "signum", "topk",
-                           "dgc_lite", "threshold"})
+    STOCHASTIC = frozenset({"qsgd", "terngrad", "randk"})
 
     def capture_graph(self, partition: Optional[Partition] = None) -> None:
         """Record one rank's whole sync step for ``partition`` (default: the pinned one) as a
         CUDA Graph; ``step()`` then replays it with one launch instead of one ctypes call
         and 1-5 kernel launches per group (the launch-bound many-small-groups case of
-        SURVEY.md §8(f)-4).  One rank and deterministic codecs only: the stochastic
-        codecs' Philox keys change every iteration and are kernel arguments.  Capturing
-        runs nothing; gradients and codec state are untouched."""
+        SURVEY.md §8(f)-4).  One rank (every codec): the stochastic codecs' Philox keys
+        derive_seed(root, rank, iteration, group) are computed on the device at the head of
+        the graph from a device iteration counter that every replay advances, and the
+        encodes read them from there.  Capturing runs nothing; gradients and codec state
+        are untouched."""
         if self.world != 1 or not self.fuse_local:
             raise ValueError("capture_graph: single-rank fused sync only")
-        if self.spec.algorithm not in self.GRAPHABLE:
-            raise ValueError(f"capture_graph: {self.spec.algorithm} draws per-iteration Philox keys")
-        from .compressors import _WS
+        from .compressors import _WS, derive_keys
 
         self.sync_host_wait()
         part = self.partition if partition is None else self._resolve(partition)
@@ -308,12 +308,18 @@ class GradSync:
                        _native.lib().mc_decode_workspace_bytes(ctypes.byref(self.cspec), grp.n, self.world))
                    for grp in plan)
         ws = _WS.get(self.device, need, self.stream)  # sized before capture: the graph keeps these pointers
+        keys = None
+        if self.spec.algorithm in self.STOCHASTIC:
+            self._dev_iter = torch.tensor([self.iteration], dtype=torch.int64, device=self.device)
+            keys = torch.zeros(len(plan), 2, dtype=torch.int64, device=self.device)
         graph = torch.cuda.CUDAGraph()
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.graph(graph, stream=self.stream):
+            if keys is not None:
+                derive_keys(self.root_seed, self.rank, self._dev_iter, keys, stream=self.stream)
             for g, grp in enumerate(plan):
-                self._sync_group(g, grp)
-        self._graph = (part.boundaries, graph, ws, len(plan))
+                self._sync_group(g, grp, None if keys is None else keys[g])
+        self._graph = (part.boundaries, graph, ws, len(plan), keys)
 
     def drop_graph(self) -> None:
         self._graph = None

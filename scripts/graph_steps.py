@@ -31,8 +31,8 @@ def timed(sync, reps=50):
 def main():
     prof = gradsets.profile("resnet50_161")
     g = torch.from_numpy(gradsets.synthetic_gradients("resnet50_161", 0, 0)).cuda()
-    for codec in ("efsignsgd", "dgc_lite", "signsgd"):
-        spec = CompressorSpec(codec, sparsity=0.999)
+    for codec in ("efsignsgd", "dgc_lite", "signsgd", "qsgd", "randk"):
+        spec = CompressorSpec(codec, sparsity=0.99 if codec == "randk" else 0.999)
         for name, part in (("naive_y8", naive_partition(prof.n_tensors, 8)),
                            ("naive_y32", naive_partition(prof.n_tensors, 32)),
                            ("layer_wise", Partition.layer_wise(prof.n_tensors))):
