@@ -100,6 +100,10 @@ typedef struct mc_layout {
   int64_t bytes;            /* total device payload size, multiple of 16 */
 } mc_layout;
 
+/* Process-wide library state: a launch counter (statistics), the SM count per device
+ * (cached), per-device flags of the kernel attributes already set (shared-memory opt-in),
+ * and the SM reserve of mc_set_sm_reserve.  No device memory is ever allocated by the
+ * library: every buffer (payloads, codec state, workspace) is the caller's. */
 int mc_abi_version(void);
 const char* mc_last_error(void); /* thread-local message of the last failing call */
 int64_t mc_kernel_launches(void); /* kernels launched by this library since load (statistics) */

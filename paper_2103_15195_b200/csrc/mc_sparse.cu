@@ -1539,11 +1539,8 @@ int encode_topk(const EncodeArgs& a, float* out) {
   note_launch(); k_topk_pass1<<<g1, 256, 0, st>>>(p);
   note_launch(); k_topk_pass2<<<(unsigned)ntiles, 256, 0, st>>>(p);
   const int h3smem = (int)(4 * (ntiles + 1));
-  static int h3_cfg = 48 * 1024;  // dynamic smem limit set so far (benign race: idempotent growth)
-  if (h3smem > h3_cfg) {
-    MC_API_CHECK(cudaFuncSetAttribute(k_topk_hist3, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (int)(H3_MAX_TILES + 1)));
-    h3_cfg = 4 * (int)(H3_MAX_TILES + 1);
-  }
+  static std::atomic<uint64_t> h3_cfg{0};  // per device: the opt-in (to the largest table) is set
+  if (h3smem > 48 * 1024) MC_API_CHECK(smem_optin(h3_cfg, k_topk_hist3, 4 * (int)(H3_MAX_TILES + 1)));
   note_launch(); k_topk_hist3<<<(unsigned)sm_count() * 2, 256, h3smem, st>>>(p, ntiles);
   // reset ticket + status for the final look-back pass (list length <= n)
   const int64_t ftiles = cdiv(n, CB_F);
