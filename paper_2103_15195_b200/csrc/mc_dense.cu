@@ -516,6 +516,99 @@ __global__ void __launch_bounds__(256) k_decode_sign_one(DP p) {
   }
 }
 
+// Byte codecs over N ranks (identity / fp16 / int8, bucket_size % 8 == 0): 8 elements per
+// thread, ranks in chunks of RC whose loads are all issued before any is used (the per-rank
+// loop of k_decode_dense leaves one rank's load in flight per thread and is latency-bound).
+// ResNet-50 set: int8 N=4/8 77 -> 57 / 132 -> 87 us, fp16 60 -> 55 / 100 -> 80 us (its HBM
+// floor: 78 us), identity N=8 138 us (floor 141).  Accumulation stays in rank order
+// (compressors.py:529-531).
+template <int ALGO>
+__global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
+  constexpr int RC = ALGO == MC_IDENTITY ? 4 : 8;
+  if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
+    const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(p.base + p.stride * threadIdx.x);
+    if (h->algorithm != p.algo || h->original_len != (uint64_t)p.n || h->n_val != p.n_val || h->n_bits != p.n_bits)
+      atomicOr(p.err, MC_ERR_HEADER);
+  }
+  const float fn = (float)p.nranks;
+  const bool pow2 = (p.nranks & (p.nranks - 1)) == 0;
+  const float inv = __fdiv_rn(1.0f, fn);
+  const uint32_t groups = (uint32_t)cdiv(p.n, 8);
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += gridDim.x * blockDim.x) {
+    const uint32_t e0 = gi * 8;
+    const int cnt = (int)imin(8, p.n - (int64_t)e0);
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+    if (cnt < 8) {  // the group's ragged end
+      for (int r = 0; r < p.nranks; ++r) {
+        float d[8];
+        dec8<ALGO, true>(p, p.base + p.stride * r, e0, cnt, d);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], d[q]);
+      }
+    } else {
+      const uint32_t b = e0 / (uint32_t)p.B;
+      for (int r0 = 0; r0 < p.nranks; r0 += RC) {
+        uint4 raw[RC][ALGO == MC_IDENTITY ? 2 : 1];
+        float sc[RC];
+#pragma unroll
+        for (int rr = 0; rr < RC; ++rr) {  // every load of the chunk first
+          if (r0 + rr >= p.nranks) break;
+          const uint8_t* pl = p.base + p.stride * (r0 + rr);
+          if (ALGO == MC_IDENTITY) {
+            const uint4* v = reinterpret_cast<const uint4*>(pl + p.off_val) + 2 * (size_t)gi;
+            raw[rr][0] = v[0];
+            raw[rr][ALGO == MC_IDENTITY ? 1 : 0] = v[1];
+          } else if (ALGO == MC_FP16) {
+            raw[rr][0] = reinterpret_cast<const uint4*>(pl + p.off_bits)[gi];
+          } else {  // int8: 8 code bytes + the bucket scale
+            const uint2 c = reinterpret_cast<const uint2*>(pl + p.off_bits)[gi];
+            raw[rr][0] = make_uint4(c.x, c.y, 0u, 0u);
+            sc[rr] = reinterpret_cast<const float*>(pl + p.off_val)[b];
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < RC; ++rr) {
+          if (r0 + rr >= p.nranks) break;
+          float d[8];
+          if (ALGO == MC_IDENTITY) {
+            const uint4 a = raw[rr][0], c = raw[rr][ALGO == MC_IDENTITY ? 1 : 0];
+            d[0] = __uint_as_float(a.x); d[1] = __uint_as_float(a.y); d[2] = __uint_as_float(a.z);
+            d[3] = __uint_as_float(a.w); d[4] = __uint_as_float(c.x); d[5] = __uint_as_float(c.y);
+            d[6] = __uint_as_float(c.z); d[7] = __uint_as_float(c.w);
+          } else if (ALGO == MC_FP16) {
+            const __half2* h2 = reinterpret_cast<const __half2*>(&raw[rr][0]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __half22float2(h2[q]);
+              d[2 * q] = f.x;
+              d[2 * q + 1] = f.y;
+            }
+          } else {
+            const float step = __fdiv_rn(sc[rr], 127.0f);  // s / 127  (:513)
+            const uint64_t w = (uint64_t)raw[rr][0].x | ((uint64_t)raw[rr][0].y << 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) d[q] = __fmul_rn((float)(int8_t)(uint8_t)(w >> (8 * q)), step);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], d[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = rank_mean(acc[q], fn, inv, pow2);
+    if (cnt == 8) {
+      reinterpret_cast<float4*>(p.out + e0)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      reinterpret_cast<float4*>(p.out + e0)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < cnt) p.out[e0 + q] = acc[q];
+    }
+  }
+}
+
 template <int ALGO, bool SAMEB>
 __global__ void __launch_bounds__(256) k_decode_dense(DP p) {
   if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
@@ -645,6 +738,18 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
       case MC_ONEBIT: k_decode_sign32<MC_ONEBIT><<<g32, 256, 0, st>>>(p); break;
       default: k_decode_sign32<MC_QSGD><<<g32, 256, 0, st>>>(p); break;
     }
+    MC_LAUNCH_CHECK();
+    return MC_OK;
+  }
+  // byte codecs with aligned sections: the chunk-prefetching kernel (alignment of every
+  // rank's sections follows from the 16-byte aligned layout and a 16-byte stride)
+  const bool aligned = stride % 16 == 0 && (uintptr_t)base % 16 == 0 && (uintptr_t)out % 16 == 0;
+  // (fp16 / identity at 2-3 ranks stay on k_decode_dense: more resident warps, measured faster)
+  if (aligned && sameb && ((a == MC_INT8 && nranks > 1) || ((a == MC_IDENTITY || a == MC_FP16) && nranks >= 4))) {
+    note_launch();
+    if (a == MC_IDENTITY) k_decode_bytes<MC_IDENTITY><<<grid, 256, 0, st>>>(p);
+    else if (a == MC_FP16) k_decode_bytes<MC_FP16><<<grid, 256, 0, st>>>(p);
+    else k_decode_bytes<MC_INT8><<<grid, 256, 0, st>>>(p);
     MC_LAUNCH_CHECK();
     return MC_OK;
   }

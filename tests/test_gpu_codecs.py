@@ -238,11 +238,13 @@ def test_serialize_deserialize_roundtrip_on_device(algo, C):
 
 
 @pytest.mark.parametrize("algo,bucket", [("efsignsgd", 512), ("efsignsgd", 384), ("onebit", 512), ("onebit", 128),
-                                         ("signsgd", 512), ("signum", 512)])
+                                         ("signsgd", 512), ("signum", 512), ("int8", 512), ("int8", 136),
+                                         ("fp16", 512), ("identity", 512), ("terngrad", 512)])
 @pytest.mark.parametrize("nranks", [2, 3, 5, 8, 9])
 def test_sign_decode_mean_many_ranks_matches_oracle(algo, bucket, nranks, C):
-    """decode_mean over 2..9 stacked sign payloads (3..8 take the per-bucket table kernel,
-    2 and 9 the per-element loop) against the oracle's rank-ordered aggregate, bit for bit.
+    """decode_mean over 2..9 stacked payloads against the oracle's rank-ordered aggregate,
+    bit for bit: sign codecs (3..8 ranks take the per-bucket table kernel, 2 and 9 the
+    per-element loop) and the byte codecs (chunk-prefetching kernel, ragged tail group).
     Ranks differ in magnitude by up to 10^4 so the f32 addition order is visible; the group
     length leaves a partial word and a partial bucket; some buckets are all zero."""
     import torch
@@ -258,8 +260,8 @@ def test_sign_decode_mean_many_ranks_matches_oracle(algo, bucket, nranks, C):
         g = (rng.standard_normal(n) * (1e-3 * 10.0 ** ((r % 5) - 2))).astype(np.float32)
         g[4096:4096 + 3 * bucket] = 0.0  # all-zero buckets (sign bit 1, scale 0)
         g[7] = -0.0
-        p, _ = C.encode(spec, torch.from_numpy(g).cuda(), None, seed=0)
-        q, _ = O.encode(spec, g, None, seed=0)
+        p, _ = C.encode(spec, torch.from_numpy(g).cuda(), None, seed=r + 1)
+        q, _ = O.encode(spec, g, None, seed=r + 1)
         pays_d.append(p)
         pays_o.append(q)
     mean_d = C.aggregate(spec, pays_d).cpu().numpy()
