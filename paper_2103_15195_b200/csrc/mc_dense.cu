@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(256) k_decode_sign_one(DP p) {
   }
 }
 
-// Byte codecs over N ranks (identity / fp16 / int8, bucket_size % 8 == 0): 8 elements per
+// Byte codecs over N ranks (identity / fp16 / int8 / terngrad, bucket_size % 8 == 0): 8 elements per
 // thread, ranks in chunks of RC whose loads are all issued before any is used (the per-rank
 // loop of k_decode_dense leaves one rank's load in flight per thread and is latency-bound).
 // ResNet-50 set: int8 N=4/8 77 -> 57 / 132 -> 87 us, fp16 60 -> 55 / 100 -> 80 us (its HBM
@@ -552,9 +552,10 @@ __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
       for (int r0 = 0; r0 < p.nranks; r0 += RC) {
         uint4 raw[RC][ALGO == MC_IDENTITY ? 2 : 1];
         float sc[RC];
+        const int nr = p.nranks - r0 < RC ? p.nranks - r0 : RC;
 #pragma unroll
         for (int rr = 0; rr < RC; ++rr) {  // every load of the chunk first
-          if (r0 + rr >= p.nranks) break;
+          if (rr >= nr) continue;
           const uint8_t* pl = p.base + p.stride * (r0 + rr);
           if (ALGO == MC_IDENTITY) {
             const uint4* v = reinterpret_cast<const uint4*>(pl + p.off_val) + 2 * (size_t)gi;
@@ -562,6 +563,10 @@ __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
             raw[rr][ALGO == MC_IDENTITY ? 1 : 0] = v[1];
           } else if (ALGO == MC_FP16) {
             raw[rr][0] = reinterpret_cast<const uint4*>(pl + p.off_bits)[gi];
+          } else if (ALGO == MC_TERNGRAD) {  // 8 two-bit codes (MSB-first) + the bucket scale
+            const uint16_t c = reinterpret_cast<const uint16_t*>(pl + p.off_bits)[gi];
+            raw[rr][0] = make_uint4((uint32_t)c, 0u, 0u, 0u);
+            sc[rr] = reinterpret_cast<const float*>(pl + p.off_val)[b];
           } else {  // int8: 8 code bytes + the bucket scale
             const uint2 c = reinterpret_cast<const uint2*>(pl + p.off_bits)[gi];
             raw[rr][0] = make_uint4(c.x, c.y, 0u, 0u);
@@ -570,7 +575,7 @@ __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
         }
 #pragma unroll
         for (int rr = 0; rr < RC; ++rr) {
-          if (r0 + rr >= p.nranks) break;
+          if (rr >= nr) continue;
           float d[8];
           if (ALGO == MC_IDENTITY) {
             const uint4 a = raw[rr][0], c = raw[rr][ALGO == MC_IDENTITY ? 1 : 0];
@@ -584,6 +589,13 @@ __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
               const float2 f = __half22float2(h2[q]);
               d[2 * q] = f.x;
               d[2 * q + 1] = f.y;
+            }
+          } else if (ALGO == MC_TERNGRAD) {  // (code - 1) * s  (:501-504)
+            const uint32_t w = raw[rr][0].x;  // byte 0 = elements 0..3, byte 1 = elements 4..7
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t code = (w >> (8 * (q >> 2) + 6 - 2 * (q & 3))) & 3u;
+              d[q] = __fmul_rn(__fsub_rn((float)code, 1.0f), sc[rr]);
             }
           } else {
             const float step = __fdiv_rn(sc[rr], 127.0f);  // s / 127  (:513)
@@ -745,10 +757,12 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
   // rank's sections follows from the 16-byte aligned layout and a 16-byte stride)
   const bool aligned = stride % 16 == 0 && (uintptr_t)base % 16 == 0 && (uintptr_t)out % 16 == 0;
   // (fp16 / identity at 2-3 ranks stay on k_decode_dense: more resident warps, measured faster)
-  if (aligned && sameb && ((a == MC_INT8 && nranks > 1) || ((a == MC_IDENTITY || a == MC_FP16) && nranks >= 4))) {
+  if (aligned && sameb && (((a == MC_INT8 || a == MC_TERNGRAD) && nranks > 1) ||
+                           ((a == MC_IDENTITY || a == MC_FP16) && nranks >= 4))) {
     note_launch();
     if (a == MC_IDENTITY) k_decode_bytes<MC_IDENTITY><<<grid, 256, 0, st>>>(p);
     else if (a == MC_FP16) k_decode_bytes<MC_FP16><<<grid, 256, 0, st>>>(p);
+    else if (a == MC_TERNGRAD) k_decode_bytes<MC_TERNGRAD><<<grid, 256, 0, st>>>(p);
     else k_decode_bytes<MC_INT8><<<grid, 256, 0, st>>>(p);
     MC_LAUNCH_CHECK();
     return MC_OK;
