@@ -941,13 +941,14 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int6
   const int64_t w = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   {  // expected offset at the window start and its variance (closed form; they only centre
-     // and size the speculated range — the chain checks it).  The range is +-(7 sd + 16), at
+     // and size the speculated range — the chain checks it).  The range is +-(6 sd + 16), at
      // most DW: early windows, whose offset is still nearly deterministic, evaluate a few
-     // dozen entering offsets instead of DW
+     // dozen entering offsets instead of DW.  A > 6 sd excursion (p ~ 2e-9 per window) hands
+     // the rest of the stream to the serial walker: slower, never wrong
     if (tid == 0) {
       double t, vv;
       randk_drift(p, w * WP, t, vv);
-      const int half = (int)ceil(7.0 * sqrt(vv)) + 16;
+      const int half = (int)ceil(6.0 * sqrt(vv)) + 16;
       const int dw = (int)imin(DW, (int64_t)((2 * half + 31) / 32 * 32));
       const int64_t L = imax(0, (int64_t)floor(t) - dw / 2);
       s_L = L;
