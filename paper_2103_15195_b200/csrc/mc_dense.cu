@@ -756,9 +756,10 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
   // byte codecs with aligned sections: the chunk-prefetching kernel (alignment of every
   // rank's sections follows from the 16-byte aligned layout and a 16-byte stride)
   const bool aligned = stride % 16 == 0 && (uintptr_t)base % 16 == 0 && (uintptr_t)out % 16 == 0;
-  // (fp16 / identity at 2-3 ranks stay on k_decode_dense: more resident warps, measured faster)
-  if (aligned && sameb && (((a == MC_INT8 || a == MC_TERNGRAD) && nranks > 1) ||
-                           ((a == MC_IDENTITY || a == MC_FP16) && nranks >= 4))) {
+  // (fp16 / identity / terngrad at 2-3 ranks stay on k_decode_dense: more resident warps,
+  // measured faster)
+  if (aligned && sameb && ((a == MC_INT8 && nranks > 1) ||
+                           ((a == MC_IDENTITY || a == MC_FP16 || a == MC_TERNGRAD) && nranks >= 4))) {
     note_launch();
     if (a == MC_IDENTITY) k_decode_bytes<MC_IDENTITY><<<grid, 256, 0, st>>>(p);
     else if (a == MC_FP16) k_decode_bytes<MC_FP16><<<grid, 256, 0, st>>>(p);
