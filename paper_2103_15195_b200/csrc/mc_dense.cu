@@ -525,6 +525,11 @@ __global__ void __launch_bounds__(256) k_decode_sign_one(DP p) {
 template <int ALGO>
 __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
   constexpr int RC = ALGO == MC_IDENTITY ? 4 : 8;
+  __shared__ float tbl[ALGO == MC_QSGD ? 256 : 1];
+  if (ALGO == MC_QSGD) {  // exact IEEE quotients code / (L-1)
+    tbl[threadIdx.x] = __fdiv_rn((float)threadIdx.x, p.top);
+    __syncthreads();
+  }
   if (blockIdx.x == 0 && threadIdx.x < p.nranks) {
     const mc_payload_header* h = reinterpret_cast<const mc_payload_header*>(p.base + p.stride * threadIdx.x);
     if (h->algorithm != p.algo || h->original_len != (uint64_t)p.n || h->n_val != p.n_val || h->n_bits != p.n_bits)
@@ -563,6 +568,10 @@ __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
             raw[rr][ALGO == MC_IDENTITY ? 1 : 0] = v[1];
           } else if (ALGO == MC_FP16) {
             raw[rr][0] = reinterpret_cast<const uint4*>(pl + p.off_bits)[gi];
+          } else if (ALGO == MC_QSGD) {  // 8 code bytes, the sign byte (MSB = first) + the scale
+            const uint2 c = reinterpret_cast<const uint2*>(pl + p.off_codes)[gi];
+            raw[rr][0] = make_uint4(c.x, c.y, (uint32_t)(pl + p.off_bits)[gi], 0u);
+            sc[rr] = reinterpret_cast<const float*>(pl + p.off_val)[b];
           } else if (ALGO == MC_TERNGRAD) {  // 8 two-bit codes (MSB-first) + the bucket scale
             const uint16_t c = reinterpret_cast<const uint16_t*>(pl + p.off_bits)[gi];
             raw[rr][0] = make_uint4((uint32_t)c, 0u, 0u, 0u);
@@ -589,6 +598,14 @@ __global__ void __launch_bounds__(256) k_decode_bytes(DP p) {
               const float2 f = __half22float2(h2[q]);
               d[2 * q] = f.x;
               d[2 * q + 1] = f.y;
+            }
+          } else if (ALGO == MC_QSGD) {  // (sign * s) * (code / (L-1))  (:470)
+            const float s = sc[rr], ns = __fmul_rn(-1.0f, s);
+            const uint32_t lo = raw[rr][0].x, hi = raw[rr][0].y, sb = raw[rr][0].z;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t code = ((q < 4 ? lo : hi) >> (8 * (q & 3))) & 0xffu;
+              d[q] = __fmul_rn(((sb >> (7 - q)) & 1u) ? s : ns, tbl[code]);
             }
           } else if (ALGO == MC_TERNGRAD) {  // (code - 1) * s  (:501-504)
             const uint32_t w = raw[rr][0].x;  // byte 0 = elements 0..3, byte 1 = elements 4..7
@@ -740,6 +757,23 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
       default: return launch_sign_tab<MC_ONEBIT>(p, st);
     }
   }
+  // byte codecs with aligned sections: the chunk-prefetching kernel (alignment of every
+  // rank's sections follows from the 16-byte aligned layout and a 16-byte stride)
+  const bool aligned = stride % 16 == 0 && (uintptr_t)base % 16 == 0 && (uintptr_t)out % 16 == 0;
+  // (fp16 / identity / terngrad at 2-3 ranks stay on k_decode_dense and 8-bit qsgd below 8
+  // ranks on k_decode_sign32: more resident warps, measured faster; qsgd at 8 ranks
+  // 122 -> 113 us on ResNet-50)
+  if (aligned && sameb && ((a == MC_INT8 && nranks > 1) || (a == MC_QSGD && p.width == 8 && nranks >= 8) ||
+                           ((a == MC_IDENTITY || a == MC_FP16 || a == MC_TERNGRAD) && nranks >= 4))) {
+    note_launch();
+    if (a == MC_QSGD) k_decode_bytes<MC_QSGD><<<grid, 256, 0, st>>>(p);
+    else if (a == MC_IDENTITY) k_decode_bytes<MC_IDENTITY><<<grid, 256, 0, st>>>(p);
+    else if (a == MC_FP16) k_decode_bytes<MC_FP16><<<grid, 256, 0, st>>>(p);
+    else if (a == MC_TERNGRAD) k_decode_bytes<MC_TERNGRAD><<<grid, 256, 0, st>>>(p);
+    else k_decode_bytes<MC_INT8><<<grid, 256, 0, st>>>(p);
+    MC_LAUNCH_CHECK();
+    return MC_OK;
+  }
   if (sign32) {
     const unsigned g32 = (unsigned)imax(1, imin(cdiv(cdiv(L.n, 32), 256), (int64_t)sm_count() * 8));
     note_launch();
@@ -750,21 +784,6 @@ int decode_mean_dense(const mc_spec* s, const mc_layout& L, const uint8_t* base,
       case MC_ONEBIT: k_decode_sign32<MC_ONEBIT><<<g32, 256, 0, st>>>(p); break;
       default: k_decode_sign32<MC_QSGD><<<g32, 256, 0, st>>>(p); break;
     }
-    MC_LAUNCH_CHECK();
-    return MC_OK;
-  }
-  // byte codecs with aligned sections: the chunk-prefetching kernel (alignment of every
-  // rank's sections follows from the 16-byte aligned layout and a 16-byte stride)
-  const bool aligned = stride % 16 == 0 && (uintptr_t)base % 16 == 0 && (uintptr_t)out % 16 == 0;
-  // (fp16 / identity / terngrad at 2-3 ranks stay on k_decode_dense: more resident warps,
-  // measured faster)
-  if (aligned && sameb && ((a == MC_INT8 && nranks > 1) ||
-                           ((a == MC_IDENTITY || a == MC_FP16 || a == MC_TERNGRAD) && nranks >= 4))) {
-    note_launch();
-    if (a == MC_IDENTITY) k_decode_bytes<MC_IDENTITY><<<grid, 256, 0, st>>>(p);
-    else if (a == MC_FP16) k_decode_bytes<MC_FP16><<<grid, 256, 0, st>>>(p);
-    else if (a == MC_TERNGRAD) k_decode_bytes<MC_TERNGRAD><<<grid, 256, 0, st>>>(p);
-    else k_decode_bytes<MC_INT8><<<grid, 256, 0, st>>>(p);
     MC_LAUNCH_CHECK();
     return MC_OK;
   }
