@@ -578,7 +578,8 @@ class GradSync:
         the step in flight so the next call overlaps it chunk by chunk (its H2D of a chunk
         waits only for this call's read-out of that chunk): the PCIe fill and drain of
         consecutive steps coincide.  ``sync_host_wait()`` (or any other step) joins them
-        into the current stream; host_out is complete after that."""
+        into the current stream; host_out is complete after that, and host_in must not be
+        rewritten before it (its H2D copies may still be in flight)."""
         if host_out is None:
             host_out = torch.empty(self.flat.numel(), dtype=torch.float32, pin_memory=True)
         if self.world == 1 and self.fuse_local and chunk_elems > 0:
