@@ -325,9 +325,18 @@ __device__ __forceinline__ float pairwise_pad32(const float* a, int L) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) B[r] = a + pad32(o) + 8 * ((k + r) >> 2);
     float v = act ? B[0][0] : 0.0f;
+    if (L > 128) {  // leaves of a split are >= 64 long: rows 1..7 always exist (inactive lanes
+                    // add in-bounds garbage nobody reads)
 #pragma unroll
-    for (int t = 1; t < 16; ++t)
-      if (8 * t < body) v = __fadd_rn(v, B[t & 3][8 * t + 8 * (t >> 2)]);
+      for (int t = 1; t < 8; ++t) v = __fadd_rn(v, B[t & 3][8 * t + 8 * (t >> 2)]);
+#pragma unroll
+      for (int t = 8; t < 16; ++t)
+        if (8 * t < body) v = __fadd_rn(v, B[t & 3][8 * t + 8 * (t >> 2)]);
+    } else {
+#pragma unroll
+      for (int t = 1; t < 16; ++t)
+        if (8 * t < body) v = __fadd_rn(v, B[t & 3][8 * t + 8 * (t >> 2)]);
+    }
     v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 1));
     v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 2));
     v = __fadd_rn(v, __shfl_xor_sync(FULL, v, 4));
