@@ -213,6 +213,23 @@ int mc_encode_push(const mc_spec* spec, const float* grad, int64_t n, double* re
 int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,
                  void* stream);
 
+/* NVLink multicast (NVLS) variant of the fused push.  mc_mcast_create builds a multicast
+ * object over `ndev` devices owned by this process (physical memory per device bound to it):
+ * mc_mcast_ptrs gives each device's unicast view (the gather buffer its decode reads) and the
+ * one multicast address.  mc_encode_push_mc encodes into `payload` (this rank's slot, unicast
+ * view) with every payload word stored ONCE through `mc_slot` (the same slot's multicast
+ * address: the store lands in every device's buffer), then releases `mc_flag` (multicast
+ * address of this rank's flag word) := epoch on every device; mc_push_wait on a device's
+ * unicast flag words then gives the gathered payloads, as with mc_encode_push.  Pipe-kernel
+ * codecs (efsignsgd, onebit, int8; bucket_size % 128 == 0). */
+typedef struct mc_mcast mc_mcast;
+int mc_mcast_create(const int32_t* devices, int32_t ndev, int64_t bytes, mc_mcast** out);
+int mc_mcast_ptrs(const mc_mcast* h, void** unicast, void** multicast, int64_t* bytes);
+void mc_mcast_destroy(mc_mcast* h);
+int mc_encode_push_mc(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+                      uint64_t key_lo, uint64_t key_hi, void* payload, void* mc_slot, uint32_t* mc_flag, uint32_t epoch,
+                      void* workspace, int64_t workspace_bytes, uint32_t* err_flags, void* stream);
+
 /* Peer exchange set-up (replaces nothing in the reference: its "allgather" is a Python list,
  * trainer.py:377-389).  mc_peer_enable: let kernels on `device` load/store memory of
  * `peer_device` (cudaDeviceEnablePeerAccess; a no-op when equal, MC_EPEER when the pair has

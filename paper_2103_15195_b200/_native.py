@@ -76,6 +76,12 @@ _SIGS = {
                                       ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_uint32, _P,
                                       ctypes.c_int64, _P, _P]),
     "mc_push_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, _P, _P]),
+    "mc_mcast_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_int64,
+                                       ctypes.POINTER(_P)]),
+    "mc_mcast_ptrs": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64)]),
+    "mc_mcast_destroy": (None, [_P]),
+    "mc_encode_push_mc": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, ctypes.c_uint64, ctypes.c_uint64, _P, _P,
+                                         _P, ctypes.c_uint32, _P, ctypes.c_int64, _P, _P]),
     "mc_derive_keys": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, _P, ctypes.c_uint64, ctypes.c_int32, _P, _P]),
     "mc_encode_dk": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, _P, _P, _P, ctypes.c_int64, _P, _P]),
     "mc_encode_decode_dk": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, _P, _P, _P, ctypes.c_int64, _P, _P,

@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libmergecomp.so"
-SOURCES = ["mc_capi.cu", "mc_bucket.cu", "mc_dense.cu", "mc_sparse.cu", "mc_sign.cu", "mc_pipe.cu"]
+SOURCES = ["mc_capi.cu", "mc_bucket.cu", "mc_dense.cu", "mc_sparse.cu", "mc_sign.cu", "mc_pipe.cu", "mc_mcast.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2", f"-I{ROOT / 'include'}"]
 # tuning experiments only (e.g. MC_NVCC_EXTRA="-DMC_RNG_ROWS=2"); never set by the product build

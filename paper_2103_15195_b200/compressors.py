@@ -315,6 +315,58 @@ def device_encode_push(spec: CompressorSpec, grad: torch.Tensor, residual: Optio
     )
 
 
+class McastBuffer:
+    """A gather buffer behind an NVLink multicast object (mc_mcast_create) over devices owned
+    by this process: ``unicast[i]`` is device i's view (what its decode reads), ``multicast``
+    the address whose stores reach every device's copy (what mc_encode_push_mc writes)."""
+
+    def __init__(self, devices: Sequence[int], nbytes: int):
+        lib = _native.lib()
+        devs = (ctypes.c_int32 * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        _native.check(lib.mc_mcast_create(devs, len(devices), int(nbytes), ctypes.byref(h)), "mc_mcast_create")
+        self._h = h
+        uc = (ctypes.c_void_p * len(devices))()
+        mcp, size = ctypes.c_void_p(), ctypes.c_int64()
+        _native.check(lib.mc_mcast_ptrs(h, uc, ctypes.byref(mcp), ctypes.byref(size)), "mc_mcast_ptrs")
+        self.unicast = [int(u) for u in uc]
+        self.multicast = int(mcp.value)
+        self.nbytes = int(size.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            torch.cuda.synchronize()
+            _native.lib().mc_mcast_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def device_encode_push_mc(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],
+                          momentum: Optional[torch.Tensor], seed: int, payload_ptr: int, mc_slot: int, mc_flag: int,
+                          epoch: int, err: Optional[torch.Tensor] = None, stream=None, cspec=None) -> None:
+    """``device_encode_push`` over a multicast buffer: every payload word is stored once
+    through ``mc_slot`` (this rank's slot, multicast address) and lands in every device's
+    copy; ``mc_flag`` (multicast address of this rank's flag word) := epoch everywhere
+    (mc_encode_push_mc).  ``payload_ptr``: the same slot's unicast address on this device."""
+    n = grad.numel()
+    cs = cspec if cspec is not None else spec.to_c()
+    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n), stream)
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=grad.device)
+    lo, hi = split_seed(seed)
+    _native.check(
+        _native.lib().mc_encode_push_mc(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum), lo, hi,
+                                        int(payload_ptr), int(mc_slot), int(mc_flag), int(epoch) & 0xFFFFFFFF,
+                                        ws.data_ptr(), ws.numel(), err.data_ptr(), _stream_ptr(stream)),
+        "mc_encode_push_mc",
+    )
+
+
 def push_wait(flags: torch.Tensor, nranks: int, epoch: int, err: Optional[torch.Tensor] = None, stream=None,
               timeout_s: float = 0.0) -> None:
     """The stream waits until all ``nranks`` local flag words equal ``epoch`` (mc_push_wait).

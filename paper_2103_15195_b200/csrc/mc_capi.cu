@@ -230,7 +230,8 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
                        uint64_t key_lo, uint64_t key_hi, void* payload, void* workspace, int64_t workspace_bytes,
                        uint32_t* err_flags, void* stream, float* out, int64_t begin = 0, int64_t count = -1,
                        int npush = 0, void* const* push_dsts = nullptr, uint32_t* const* push_flags = nullptr,
-                       uint32_t epoch = 0, const uint64_t* dkey = nullptr) {
+                       uint32_t epoch = 0, const uint64_t* dkey = nullptr, void* mc_dst = nullptr,
+                       uint32_t* mc_flag = nullptr) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
   if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
@@ -263,6 +264,8 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
   a.push_flags = push_flags;
   a.epoch = epoch;
   a.dkey = dkey;
+  a.mc_dst = mc_dst;
+  a.mc_flag = mc_flag;
   if (begin != 0 || (count >= 0 && count != n)) {  // chunked: deterministic elementwise / bucketed codecs only
     const int al = s->algorithm;
     if (begin < 0 || count < 1 || begin + count > n) { set_error("bad chunk [%lld, +%lld)", (long long)begin, (long long)count); return MC_EINVAL; }
@@ -429,6 +432,21 @@ int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* resid
   a.epoch = epoch;
   return launch_push_copy(static_cast<const uint8_t*>(payload), L.bytes, a, static_cast<cudaStream_t>(stream),
                           s->algorithm == MC_THRESHOLD ? &L : nullptr);
+}
+
+int mc_encode_push_mc(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                      uint64_t key_lo, uint64_t key_hi, void* payload, void* mc_slot, uint32_t* mc_flag, uint32_t epoch,
+                      void* workspace, int64_t workspace_bytes, uint32_t* err_flags, void* stream) {
+  if (!payload || !mc_slot || !mc_flag) { set_error("null payload / multicast slot / flag"); return MC_EINVAL; }
+  void* dsts[1] = {payload};
+  uint32_t* flags[1] = {mc_flag};
+  const int rc = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
+                             err_flags, stream, nullptr, 0, -1, 1, dsts, flags, epoch, nullptr, mc_slot, mc_flag);
+  if (rc == MC_FUSED_UNSUPPORTED) {
+    set_error("the multicast push needs an aligned efsignsgd / onebit / int8 group (bucket_size %% 128 == 0)");
+    return MC_EINVAL;
+  }
+  return rc;
 }
 
 int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,

@@ -561,6 +561,9 @@ struct EncodeArgs {
   // graph-capturable keys (mc_encode_dk / mc_encode_decode_dk): the 128-bit Philox key is
   // read on the device from dkey[0..1] (written by mc_derive_keys) instead of (k0, k1)
   const uint64_t* dkey = nullptr;
+  // NVLS multicast push (mc_encode_push_mc): multicast address of this rank's slot and flag
+  void* mc_dst = nullptr;
+  uint32_t* mc_flag = nullptr;
 };
 
 constexpr int MC_MAX_PUSH = 16;

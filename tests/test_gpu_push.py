@@ -89,3 +89,80 @@ def test_merge_stage_pack_unpack(case):
     torch.cuda.synchronize()
     for o, s in zip(outs, srcs):
         assert torch.equal(o, s * 2)
+
+
+class _Ptr:
+    """A raw device address with the tensor interface the decode wrappers read."""
+
+    def __init__(self, addr):
+        self.addr = addr
+
+    def data_ptr(self):
+        return self.addr
+
+
+@pytest.mark.parametrize("algo", ["efsignsgd", "onebit", "int8"])
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+def test_multicast_push_equals_allgather(algo, nranks):
+    """The NVLS push (mc_encode_push_mc): one multicast object on this GPU holds the gather
+    buffer and the flag words; N simulated ranks each store their payload ONCE through
+    their slot's multicast address (multimem.st) and release their flag the same way.  The
+    device's unicast view must equal, byte for byte, the rank-ordered concatenation of
+    independently encoded payloads, the flags must carry the epoch, and the decode must
+    equal the plain decode_mean."""
+    from cuda.bindings import runtime as cudart
+
+    from paper_2103_15195_b200 import _native
+    from paper_2103_15195_b200 import compressors as C
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    spec = CompressorSpec(algo)
+    n = 1_048_576 + 512 * 7 + 13
+    L = _native.layout(spec.to_c(), n)
+    stride = (L.bytes + 15) // 16 * 16
+    foff = nranks * stride
+    try:
+        buf = C.McastBuffer([0], foff + 4 * nranks)
+    except _native.NativeError as exc:  # e.g. cuMulticastCreate rejected (no NVLS fabric on this box)
+        pytest.skip(f"multicast objects unavailable here: {exc}")
+    cudart.cudaMemset(buf.unicast[0], 0, buf.nbytes)
+    gens = [torch.Generator(device="cuda").manual_seed(500 + r) for r in range(nranks)]
+    grads = [torch.randn(n, device="cuda", generator=g) * 1e-3 for g in gens]
+    ef = spec.uses_error_feedback
+    res_a = [torch.zeros(n, dtype=torch.float64, device="cuda") if ef else None for _ in range(nranks)]
+    res_b = [torch.zeros(n, dtype=torch.float64, device="cuda") if ef else None for _ in range(nranks)]
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    try:
+        for epoch in (1, 2):
+            for r in range(nranks):
+                C.device_encode_push_mc(spec, grads[r] * epoch, res_a[r], None, 1, buf.unicast[0] + r * stride,
+                                        buf.multicast + r * stride, buf.multicast + foff + 4 * r, epoch, err)
+            flags = torch.empty(nranks, dtype=torch.int32, device="cuda")
+            C.push_wait(_FlagView(buf.unicast[0] + foff), nranks, epoch, err, timeout_s=20.0)
+            got = torch.empty(foff, dtype=torch.uint8, device="cuda")
+            torch.cuda.synchronize()
+            cudart.cudaMemcpy(got.data_ptr(), buf.unicast[0], foff, cudart.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+            cudart.cudaMemcpy(flags.data_ptr(), buf.unicast[0] + foff, 4 * nranks,
+                              cudart.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+            ref = torch.zeros(foff, dtype=torch.uint8, device="cuda")
+            for r in range(nranks):
+                C.device_encode(spec, grads[r] * epoch, res_b[r], None, 1, out=ref[r * stride:r * stride + L.bytes])
+            torch.cuda.synchronize()
+            assert int(err.item()) == 0
+            assert bool((flags == epoch).all())
+            for r in range(nranks):  # payload bytes of every slot (the slot tails are padding)
+                assert torch.equal(got[r * stride:r * stride + L.bytes], ref[r * stride:r * stride + L.bytes]), (algo, r)
+            if ef:
+                for r in range(nranks):
+                    assert torch.equal(res_a[r].view(torch.int64), res_b[r].view(torch.int64))
+            o1, o2 = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+            C.device_decode_mean(spec, _Ptr(buf.unicast[0]), stride, nranks, n, o1, err)
+            C.device_decode_mean(spec, ref, stride, nranks, n, o2, err)
+            torch.cuda.synchronize()
+            assert torch.equal(o1.view(torch.int32), o2.view(torch.int32))
+    finally:
+        buf.close()
+
+
+class _FlagView(_Ptr):
+    device = torch.device("cuda", 0)
