@@ -2,6 +2,8 @@
 
     compute-sanitizer --tool memcheck python scripts/sanitize_codecs.py
     compute-sanitizer --tool racecheck python scripts/sanitize_codecs.py --small
+
+Round 2: 3- and 8-worker aggregates (table / prefetching decodes) and device-key encodes.
 """
 import sys
 from pathlib import Path
@@ -23,10 +25,19 @@ for algo in ALGORITHMS:
             x = torch.from_numpy((rng.standard_normal(n) * 1e-3).astype(np.float32)).cuda()
             st = None
             pays = []
-            for w in range(2):
+            for w in range(8 if n == sizes[-1] else 2):  # 8 workers: the 3..8-rank decode kernels
                 p, st = C.encode(spec, x * (w + 1), st, seed=C.derive_seed(1, w, 0, 0))
                 pays.append(p)
-            C.aggregate(spec, pays)
+            C.aggregate(spec, pays[:2])
+            if len(pays) > 2:
+                C.aggregate(spec, pays[:3])
+                C.aggregate(spec, pays)
+            # graph-mode keys: the Philox key derived and read on the device
+            it = torch.zeros(1, dtype=torch.int64, device="cuda")
+            keys = torch.zeros(2, 2, dtype=torch.int64, device="cuda")
+            C.derive_keys(1, 0, it, keys)
+            C.device_encode(spec, x, None if st is None else st.residual, None if st is None else st.momentum, 0,
+                            dkey=keys[0])
             out = torch.empty_like(x)
             C.device_encode_decode(spec, x.clone(), None if st is None else st.residual,
                                    None if st is None else st.momentum, 7, out)
