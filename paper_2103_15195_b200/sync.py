@@ -515,6 +515,8 @@ class GradSync:
         if graph is not None and graph[0] == part.boundaries:
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.stream(self.stream):
+                if graph[4] is not None:  # the graph's key schedule starts from the host iteration
+                    self._dev_iter.fill_(self.iteration)  # (eager steps may have run in between)
                 graph[1].replay()
             torch.cuda.current_stream(self.device).wait_stream(self.stream)
             self.iteration += 1

@@ -232,10 +232,16 @@ def test_graph_replay_equals_eager_steps(algo):
     a.step()  # one eager step first: the graph continues the iteration count from the host
     b.step()
     a.capture_graph()
-    for it in range(3):
+    other = naive_partition(prof.n_tensors, 3)
+    for it in range(4):
         g = torch.from_numpy(gradsets.synthetic_gradients("resnet50_161", it, 0)).cuda()
         a.flat.copy_(g)
         b.flat.copy_(g)
+        if it == 2:  # an eager step of another partition in between: the keys follow the iteration
+            a.step(other)
+            b.step(other)
+            a.flat.copy_(g)
+            b.flat.copy_(g)
         a.step()
         b.step()
         torch.cuda.synchronize()
