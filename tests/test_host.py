@@ -216,3 +216,32 @@ def test_bench_cli_parses():
     r = subprocess.run([sys.executable, str(root / "bench.py"), "--help"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "--e2e-chunk" in r.stdout
+
+
+def test_chunk_ranges_cover_group_on_bucket_and_word_boundaries():
+    """GradSync's N > 1 chunk pipeline: chunks tile the group exactly, every chunk but the
+    last is a multiple of lcm(bucket_size, 32) (so chunk-wise encodes equal the whole-group
+    encode), automatic only for the byte codecs and only for groups >= 2 CHUNK_MIN."""
+    import math
+    from types import SimpleNamespace
+
+    from paper_2103_15195_b200.spec import CompressorSpec
+    from paper_2103_15195_b200.sync import GradSync
+
+    def ranges(algo, n, world=2, chunk=None, bucket=512):
+        obj = SimpleNamespace(world=world, chunk_elems=chunk, spec=CompressorSpec(algo, bucket_size=bucket),
+                              CHUNKABLE=GradSync.CHUNKABLE, CHUNK_AUTO=GradSync.CHUNK_AUTO,
+                              CHUNK_MIN=GradSync.CHUNK_MIN)
+        return GradSync._chunk_ranges(obj, n)
+
+    assert ranges("int8", 25_557_032, world=1) is None               # one rank: nothing to overlap
+    assert ranges("efsignsgd", 25_557_032) is None                   # 1-bit codecs: not by default
+    assert ranges("qsgd", 25_557_032, chunk=1 << 20) is None         # stream offsets span the group
+    assert ranges("int8", 3_000_000) is None                         # small group
+    for algo, n, chunk, bucket in [("int8", 25_557_032, None, 512), ("fp16", 44_555_013, None, 512),
+                                   ("efsignsgd", 100_003, 1024, 512), ("onebit", 100_003, 1000, 50)]:
+        r = ranges(algo, n, chunk=chunk, bucket=bucket)
+        assert r is not None and r[0][0] == 0 and r[-1][1] == n
+        align = bucket * 32 // math.gcd(bucket, 32)
+        for (a, b), (c, _) in zip(r, r[1:]):
+            assert b == c and (b - a) % align == 0
