@@ -212,6 +212,17 @@ int mc_encode_push(const mc_spec* spec, const float* grad, int64_t n, double* re
                    void* stream);
 int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t timeout_ns, uint32_t* err_flags,
                  void* stream);
+/* The same two calls with every per-step scalar read on the device, for a CUDA Graph of the
+ * whole exchange step at N > 1: `epoch` points to the device word holding the exchange epoch
+ * (the caller rewrites it before each replay), `dkey` to the Philox key (uint64[2], written by
+ * mc_derive_keys at the head of the graph) — required by the codecs that draw random numbers
+ * (randk, qsgd, terngrad), ignored (may be NULL) by the others. */
+int mc_encode_push_dev(const mc_spec* spec, const float* grad, int64_t n, double* residual, float* momentum,
+                       const uint64_t* dkey, void* payload, void* const* dsts, uint32_t* const* flags, int32_t nranks,
+                       const uint32_t* epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                       void* stream);
+int mc_push_wait_dev(const uint32_t* flags, int32_t nranks, const uint32_t* epoch, uint64_t timeout_ns,
+                     uint32_t* err_flags, void* stream);
 
 /* NVLink multicast (NVLS) variant of the fused push.  mc_mcast_create builds a multicast
  * object over `ndev` devices owned by this process (physical memory per device bound to it):

@@ -76,6 +76,9 @@ _SIGS = {
                                       ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_uint32, _P,
                                       ctypes.c_int64, _P, _P]),
     "mc_push_wait": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, _P, _P]),
+    "mc_encode_push_dev": (ctypes.c_int, [_SPEC, _P, ctypes.c_int64, _P, _P, _P, _P, ctypes.POINTER(_P),
+                                          ctypes.POINTER(_P), ctypes.c_int32, _P, _P, ctypes.c_int64, _P, _P]),
+    "mc_push_wait_dev": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_uint64, _P, _P]),
     "mc_mcast_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_int64,
                                        ctypes.POINTER(_P)]),
     "mc_mcast_ptrs": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64)]),

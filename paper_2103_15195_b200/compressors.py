@@ -315,6 +315,35 @@ def device_encode_push(spec: CompressorSpec, grad: torch.Tensor, residual: Optio
     )
 
 
+def device_encode_push_dev(spec: CompressorSpec, grad: torch.Tensor, residual: Optional[torch.Tensor],
+                           momentum: Optional[torch.Tensor], dkey: Optional[torch.Tensor], payload: torch.Tensor,
+                           dsts: Sequence[int], flags: Sequence[int], epoch: torch.Tensor,
+                           err: torch.Tensor, stream=None, cspec=None) -> None:
+    """``device_encode_push`` with the Philox key (``dkey``, device int64[2]; None for codecs
+    that draw no random numbers) and the exchange epoch (``epoch``, device int32[1]) read on
+    the device (mc_encode_push_dev): the form a CUDA Graph of the N > 1 step replays."""
+    n = grad.numel()
+    cs = cspec if cspec is not None else spec.to_c()
+    ws = _WS.get(grad.device, _native.workspace_bytes(cs, n), stream)
+    k = len(dsts)
+    arr_d = (ctypes.c_void_p * k)(*dsts)
+    arr_f = (ctypes.c_void_p * k)(*flags)
+    _native.check(
+        _native.lib().mc_encode_push_dev(ctypes.byref(cs), grad.data_ptr(), n, _ptr(residual), _ptr(momentum),
+                                         _ptr(dkey), payload.data_ptr(), arr_d, arr_f, k, epoch.data_ptr(),
+                                         ws.data_ptr(), ws.numel(), err.data_ptr(), _stream_ptr(stream)),
+        "mc_encode_push_dev",
+    )
+
+
+def push_wait_dev(flags: torch.Tensor, nranks: int, epoch: torch.Tensor, err: torch.Tensor, stream=None,
+                  timeout_s: float = 0.0) -> None:
+    """``push_wait`` against the epoch held in the device word ``epoch`` (mc_push_wait_dev)."""
+    _native.check(_native.lib().mc_push_wait_dev(flags.data_ptr(), nranks, epoch.data_ptr(), int(timeout_s * 1e9),
+                                                 err.data_ptr(), _stream_ptr(stream)),
+                  "mc_push_wait_dev")
+
+
 class McastBuffer:
     """A gather buffer behind an NVLink multicast object (mc_mcast_create) over devices owned
     by this process: ``unicast[i]`` is device i's view (what its decode reads), ``multicast``

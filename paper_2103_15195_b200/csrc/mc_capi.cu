@@ -231,7 +231,7 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
                        uint32_t* err_flags, void* stream, float* out, int64_t begin = 0, int64_t count = -1,
                        int npush = 0, void* const* push_dsts = nullptr, uint32_t* const* push_flags = nullptr,
                        uint32_t epoch = 0, const uint64_t* dkey = nullptr, void* mc_dst = nullptr,
-                       uint32_t* mc_flag = nullptr) {
+                       uint32_t* mc_flag = nullptr, const uint32_t* epoch_ptr = nullptr) {
   if (!spec_ok(s)) return MC_EINVAL;
   if (n < 1) { set_error("gradient must have at least one element"); return MC_EINVAL; }
   if (!grad || !payload || !err_flags) { set_error("null device pointer"); return MC_EINVAL; }
@@ -266,6 +266,7 @@ static int encode_impl(const mc_spec* s, const float* grad, int64_t n, double* r
   a.dkey = dkey;
   a.mc_dst = mc_dst;
   a.mc_flag = mc_flag;
+  a.epoch_ptr = epoch_ptr;
   if (begin != 0 || (count >= 0 && count != n)) {  // chunked: deterministic elementwise / bucketed codecs only
     const int al = s->algorithm;
     if (begin < 0 || count < 1 || begin + count > n) { set_error("bad chunk [%lld, +%lld)", (long long)begin, (long long)count); return MC_EINVAL; }
@@ -312,6 +313,7 @@ struct PushArgs {
   uint8_t* dst[MC_MAX_PUSH];
   uint32_t* flag[MC_MAX_PUSH];
   uint32_t epoch;
+  const uint32_t* epoch_ptr;  // device-resident epoch (graph replay) or null: `epoch`
   uint32_t* done;
   int64_t off_idx, off_val;  // sparse (threshold): only the header and the first n_idx entries move
   int sparse;
@@ -344,7 +346,8 @@ __global__ void __launch_bounds__(256) k_push_copy(PushArgs a) {
   if (last_cta(a.done)) {
     if (threadIdx.x == 0) {
       __threadfence_system();
-      for (int j = 0; j < a.nflag; ++j) st_release_sys(a.flag[j], a.epoch);
+      const uint32_t ep = a.epoch_ptr ? *a.epoch_ptr : a.epoch;
+      for (int j = 0; j < a.nflag; ++j) st_release_sys(a.flag[j], ep);
     }
   }
 }
@@ -352,7 +355,9 @@ __global__ void __launch_bounds__(256) k_push_copy(PushArgs a) {
 // Bounded: a peer silent for timeout_ns sets MC_ERR_PEER_TIMEOUT and TRAPS — the context
 // faults and the job fails loudly (like NCCL's watchdog abort) instead of decoding stale or
 // half-written slots and losing the double-buffer invariant.
-__global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch, uint64_t timeout_ns, uint32_t* err) {
+__global__ void k_push_wait(const uint32_t* flags, int n, uint32_t epoch0, const uint32_t* epoch_ptr,
+                            uint64_t timeout_ns, uint32_t* err) {
+  const uint32_t epoch = epoch_ptr ? *epoch_ptr : epoch0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     uint64_t t0 = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -398,6 +403,7 @@ int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a,
     if (a.push_dsts[j] != (void*)payload) pa.dst[pa.ndst++] = static_cast<uint8_t*>(a.push_dsts[j]);
   }
   pa.epoch = a.epoch;
+  pa.epoch_ptr = a.epoch_ptr;
   pa.done = reinterpret_cast<uint32_t*>(a.ws);  // the encode is complete in stream order: its scratch is free
   MC_API_CHECK(cudaMemsetAsync(pa.done, 0, 4, st));
   const unsigned g = (unsigned)imax(1, imin(cdiv(pa.bytes / 16, 256), (int64_t)sm_count() * 4));
@@ -410,17 +416,18 @@ int launch_push_copy(const uint8_t* payload, int64_t bytes, const EncodeArgs& a,
 
 extern "C" {
 
-int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
-                   uint64_t key_lo, uint64_t key_hi, void* payload, void* const* dsts, uint32_t* const* flags,
-                   int32_t nranks, uint32_t epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
-                   void* stream) {
+static int encode_push_impl(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                            uint64_t key_lo, uint64_t key_hi, const uint64_t* dkey, void* payload, void* const* dsts,
+                            uint32_t* const* flags, int32_t nranks, uint32_t epoch, const uint32_t* epoch_ptr,
+                            void* workspace, int64_t workspace_bytes, uint32_t* err_flags, void* stream) {
   if (nranks < 1 || nranks > MC_MAX_PUSH || !dsts || !flags) { set_error("bad push destinations"); return MC_EINVAL; }
   const int rc = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
-                             err_flags, stream, nullptr, 0, -1, nranks, dsts, flags, epoch);
+                             err_flags, stream, nullptr, 0, -1, nranks, dsts, flags, epoch, dkey, nullptr, nullptr,
+                             epoch_ptr);
   if (rc != MC_FUSED_UNSUPPORTED) return rc;
   // this codec's kernels do not push: plain encode, then the peer copy + flags
   const int rc2 = encode_impl(s, grad, n, residual, momentum, key_lo, key_hi, payload, workspace, workspace_bytes,
-                              err_flags, stream, nullptr);
+                              err_flags, stream, nullptr, 0, -1, 0, nullptr, nullptr, 0, dkey);
   if (rc2 != MC_OK) return rc2;
   mc_layout L;
   if (fill_layout(s, n, 0, &L) != MC_OK) return MC_EINVAL;
@@ -430,8 +437,30 @@ int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* resid
   a.push_dsts = dsts;
   a.push_flags = flags;
   a.epoch = epoch;
+  a.epoch_ptr = epoch_ptr;
   return launch_push_copy(static_cast<const uint8_t*>(payload), L.bytes, a, static_cast<cudaStream_t>(stream),
                           s->algorithm == MC_THRESHOLD ? &L : nullptr);
+}
+
+int mc_encode_push(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                   uint64_t key_lo, uint64_t key_hi, void* payload, void* const* dsts, uint32_t* const* flags,
+                   int32_t nranks, uint32_t epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                   void* stream) {
+  return encode_push_impl(s, grad, n, residual, momentum, key_lo, key_hi, nullptr, payload, dsts, flags, nranks, epoch,
+                          nullptr, workspace, workspace_bytes, err_flags, stream);
+}
+
+int mc_encode_push_dev(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
+                       const uint64_t* dkey, void* payload, void* const* dsts, uint32_t* const* flags, int32_t nranks,
+                       const uint32_t* epoch, void* workspace, int64_t workspace_bytes, uint32_t* err_flags,
+                       void* stream) {
+  if (!epoch) { set_error("null device epoch"); return MC_EINVAL; }
+  if (s && !dkey && (s->algorithm == MC_RANDK || s->algorithm == MC_QSGD || s->algorithm == MC_TERNGRAD)) {
+    set_error("mc_encode_push_dev: this codec draws random numbers and needs a device key");
+    return MC_EINVAL;
+  }
+  return encode_push_impl(s, grad, n, residual, momentum, 0, 0, dkey, payload, dsts, flags, nranks, 0, epoch,
+                          workspace, workspace_bytes, err_flags, stream);
 }
 
 int mc_encode_push_mc(const mc_spec* s, const float* grad, int64_t n, double* residual, float* momentum,
@@ -454,7 +483,17 @@ int mc_push_wait(const uint32_t* flags, int32_t nranks, uint32_t epoch, uint64_t
   if (!flags || nranks < 1 || !err_flags) { set_error("bad flags"); return MC_EINVAL; }
   if (timeout_ns == 0) timeout_ns = MC_PUSH_TIMEOUT_DEFAULT_NS;
   note_launch();
-  k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, epoch, timeout_ns, err_flags);
+  k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, epoch, nullptr, timeout_ns, err_flags);
+  MC_LAUNCH_CHECK();
+  return MC_OK;
+}
+
+int mc_push_wait_dev(const uint32_t* flags, int32_t nranks, const uint32_t* epoch, uint64_t timeout_ns,
+                     uint32_t* err_flags, void* stream) {
+  if (!flags || nranks < 1 || !err_flags || !epoch) { set_error("bad flags"); return MC_EINVAL; }
+  if (timeout_ns == 0) timeout_ns = MC_PUSH_TIMEOUT_DEFAULT_NS;
+  note_launch();
+  k_push_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, nranks, 0, epoch, timeout_ns, err_flags);
   MC_LAUNCH_CHECK();
   return MC_OK;
 }

@@ -564,6 +564,8 @@ struct EncodeArgs {
   // NVLS multicast push (mc_encode_push_mc): multicast address of this rank's slot and flag
   void* mc_dst = nullptr;
   uint32_t* mc_flag = nullptr;
+  // graph capture at N > 1: the exchange epoch read on the device (nullptr: `epoch`)
+  const uint32_t* epoch_ptr = nullptr;
 };
 
 constexpr int MC_MAX_PUSH = 16;

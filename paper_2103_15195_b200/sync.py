@@ -291,13 +291,20 @@ class GradSync:
         """Record one rank's whole sync step for ``partition`` (default: the pinned one) as a
         CUDA Graph; ``step()`` then replays it with one launch instead of one ctypes call
         and 1-5 kernel launches per group (the launch-bound many-small-groups case of
-        SURVEY.md §8(f)-4).  One rank (every codec): the stochastic codecs' Philox keys
-        derive_seed(root, rank, iteration, group) are computed on the device at the head of
-        the graph from a device iteration counter that every replay advances, and the
-        encodes read them from there.  Capturing runs nothing; gradients and codec state
-        are untouched."""
-        if self.world != 1 or not self.fuse_local:
-            raise ValueError("capture_graph: single-rank fused sync only")
+        SURVEY.md §8(f)-4).  The stochastic codecs' Philox keys derive_seed(root, rank,
+        iteration, group) are computed on the device at the head of the graph from a device
+        iteration counter that every replay advances, and the encodes read them from there.
+
+        One rank: the fused encode+decode of every group (every codec).  Several ranks with
+        the peer exchange (``use_peer_exchange`` / ``try_peer_exchange``): the whole exchange
+        step — encode+push of every group, then wait+decode — with the exchange epoch read
+        from a device word (mc_encode_push_dev / mc_push_wait_dev) that ``step()`` rewrites
+        before each replay; two graphs, one per gather-buffer parity, alternate.  The peer
+        buffers are created (a collective: every rank calls this) before capturing.
+        Capturing runs nothing; gradients and codec state are untouched."""
+        peer = self.world > 1 and getattr(self, "_peer", None) is not None
+        if not peer and (self.world != 1 or not self.fuse_local):
+            raise ValueError("capture_graph: single-rank fused sync or the peer exchange only")
         from .compressors import _WS, derive_keys
 
         self.sync_host_wait()
@@ -312,14 +319,25 @@ class GradSync:
         if self.spec.algorithm in self.STOCHASTIC:
             self._dev_iter = torch.tensor([self.iteration], dtype=torch.int64, device=self.device)
             keys = torch.zeros(len(plan), 2, dtype=torch.int64, device=self.device)
-        graph = torch.cuda.CUDAGraph()
-        self.stream.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.graph(graph, stream=self.stream):
-            if keys is not None:
-                derive_keys(self.root_seed, self.rank, self._dev_iter, keys, stream=self.stream)
+        dep = None
+        if peer:
             for g, grp in enumerate(plan):
-                self._sync_group(g, grp, None if keys is None else keys[g])
-        self._graph = (part.boundaries, graph, ws, len(plan), keys)
+                self._peer_group(part.boundaries, g, grp)
+            dep = torch.zeros(1, dtype=torch.int32, device=self.device)
+        graphs = []
+        for par in ((0, 1) if peer else (None,)):
+            graph = torch.cuda.CUDAGraph()
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.graph(graph, stream=self.stream):
+                if keys is not None:
+                    derive_keys(self.root_seed, self.rank, self._dev_iter, keys, stream=self.stream)
+                if peer:
+                    self._step_peer(plan, part.boundaries, cap=(par, dep, keys))
+                else:
+                    for g, grp in enumerate(plan):
+                        self._sync_group(g, grp, None if keys is None else keys[g])
+            graphs.append(graph)
+        self._graph = (part.boundaries, graphs if peer else graphs[0], ws, len(plan), keys, dep)
 
     def drop_graph(self) -> None:
         self._graph = None
@@ -479,25 +497,37 @@ class GradSync:
             self._peer["groups"][(key, g)] = st
         return st
 
-    def _step_peer(self, plan, key) -> None:
-        from .compressors import device_encode_push, push_wait
+    def _step_peer(self, plan, key, cap=None) -> None:
+        """``cap`` = (parity, device epoch word, device keys or None) while capturing a graph."""
+        from .compressors import device_encode_push, device_encode_push_dev, push_wait, push_wait_dev
 
-        self._peer["epoch"] += 1
-        ep = self._peer["epoch"]
-        par = ep & 1
+        if cap is None:
+            self._peer["epoch"] += 1
+            ep = self._peer["epoch"]
+            par = ep & 1
+        else:
+            par, dep, keys = cap
         pend = []
         for g, grp in enumerate(plan):  # every encode pushes as it finishes: no collective launch
             st = self._peer_group(key, g, grp)
-            lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
             buf = st["bufs"][par]
             own = buf[self.rank * st["stride"]:(self.rank + 1) * st["stride"]]
-            device_encode_push(self.spec, self.flat[grp.start:grp.end], grp.residual, grp.momentum, lo | (hi << 64),
-                               own, st["dsts"][par], st["flags"][par], ep, err=self.err, stream=self.stream,
-                               cspec=self.cspec)
+            x = self.flat[grp.start:grp.end]
+            if cap is None:
+                lo, hi = _native.derive_key(self.root_seed, self.rank, self.iteration, g)
+                device_encode_push(self.spec, x, grp.residual, grp.momentum, lo | (hi << 64), own, st["dsts"][par],
+                                   st["flags"][par], ep, err=self.err, stream=self.stream, cspec=self.cspec)
+            else:
+                device_encode_push_dev(self.spec, x, grp.residual, grp.momentum, None if keys is None else keys[g],
+                                       own, st["dsts"][par], st["flags"][par], dep, self.err, stream=self.stream,
+                                       cspec=self.cspec)
             pend.append((grp, st, buf))
         for grp, st, buf in pend:
-            push_wait(st["fl"][par * self.world:(par + 1) * self.world], self.world, ep, err=self.err,
-                      stream=self.stream)
+            fl = st["fl"][par * self.world:(par + 1) * self.world]
+            if cap is None:
+                push_wait(fl, self.world, ep, err=self.err, stream=self.stream)
+            else:
+                push_wait_dev(fl, self.world, dep, self.err, stream=self.stream)
             device_decode_mean(self.spec, buf, st["stride"], self.world, grp.n, self.flat[grp.start:grp.end],
                                self.err, stream=self.stream, cspec=self.cspec)
 
@@ -517,7 +547,13 @@ class GradSync:
             with torch.cuda.stream(self.stream):
                 if graph[4] is not None:  # the graph's key schedule starts from the host iteration
                     self._dev_iter.fill_(self.iteration)  # (eager steps may have run in between)
-                graph[1].replay()
+                if graph[5] is not None:  # peer exchange: this step's epoch, the graph of its parity
+                    self._peer["epoch"] += 1
+                    ep = self._peer["epoch"] & 0xFFFFFFFF
+                    graph[5].fill_(ep - (1 << 32) if ep >= 1 << 31 else ep)
+                    graph[1][ep & 1].replay()
+                else:
+                    graph[1].replay()
             torch.cuda.current_stream(self.device).wait_stream(self.stream)
             self.iteration += 1
             return

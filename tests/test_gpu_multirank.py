@@ -50,10 +50,12 @@ def _rank(rank, world, port, kw, q, peer=False):
             if not all(g.chunks for g in sync._plan(sync.partition)[1:]):
                 q.put((rank, "groups were not chunked"))
                 return
-        elif peer == "probe":  # the production entry: store-then-readback probe, then push
+        elif peer in ("probe", "graph"):  # the production entry: store-then-readback probe, then push
             if not sync.try_peer_exchange():
                 q.put((rank, "peer probe failed"))
                 return
+            if peer == "graph":  # the whole exchange step as two CUDA Graphs (epoch parity)
+                sync.capture_graph()
         elif peer:
             try:
                 sync.use_peer_exchange()
@@ -65,7 +67,11 @@ def _rank(rank, world, port, kw, q, peer=False):
         for it in range(3):
             sync.flat.copy_(torch.from_numpy(gradsets.synthetic_gradients("tiny40", it, rank)))
             torch.cuda.synchronize()
-            if peer in (True, "probe") and it > 0:  # the peer step: no host synchronisation, no allocation
+            if peer == "graph" and it == 1:  # an eager peer step between replays: epochs stay in step
+                graph, sync._graph = sync._graph, None
+                sync.step()
+                sync._graph = graph
+            elif peer in (True, "probe", "graph") and it > 0:  # no host synchronisation, no allocation
                 a0 = torch.cuda.memory_stats(0).get("allocation.all.allocated", 0)
                 torch.cuda.set_sync_debug_mode("error")
                 try:
@@ -95,6 +101,15 @@ def test_two_ranks_match_oracle(kw, peer):
     both ranks; peer-probe: the same reached through try_peer_exchange (peer access enabled,
     one store-then-readback probe kernel per rank) as bench.py does."""
     _run_pair(kw, peer)
+
+
+@pytest.mark.parametrize("kw", SPECS, ids=lambda k: k["algorithm"])
+def test_two_ranks_peer_graph_matches_oracle(kw):
+    """The N > 1 exchange step captured as CUDA Graphs (capture_graph with the peer exchange:
+    epoch and stochastic keys read from device words, one graph per buffer parity), replayed
+    for iterations 0 and 2 around an eager peer step at iteration 1, equals the oracle's
+    2-worker Trainer.step loop bit for bit; replays neither synchronise nor allocate."""
+    _run_pair(kw, "graph")
 
 
 def _run_pair(kw, peer):
