@@ -7,6 +7,7 @@
 // equal |x| at the k-th boundary the LOWEST indices are kept.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "mc_internal.cuh"
@@ -674,6 +675,7 @@ struct RP {
   uint8_t* payload;
   mc_payload_header hdr;
   const uint64_t* dkey;  // device-resident Philox key (graph capture) or null: (k0, k1)
+  float band_sig;        // speculated entering offsets: expectation +- (band_sig sd + 16)
 };
 __device__ __forceinline__ Philox randk_philox(const RP& p) {
   return p.dkey ? Philox{p.dkey[0], p.dkey[1]} : Philox{p.k0, p.k1};
@@ -682,8 +684,25 @@ __device__ __forceinline__ Philox randk_philox(const RP& p) {
 __device__ __forceinline__ uint32_t draw32(const Philox& ph, uint64_t pos) {
   uint64_t w[4];
   ph.block(pos >> 3, w);
-  const uint64_t x = w[(pos >> 1) & 3];
+  const unsigned q = (unsigned)(pos >> 1) & 3u;  // selects, not a dynamically indexed (local) array
+  const uint64_t x = q == 0 ? w[0] : q == 1 ? w[1] : q == 2 ? w[2] : w[3];
   return (pos & 1) ? (uint32_t)(x >> 32) : (uint32_t)x;
+}
+
+__device__ __forceinline__ uint32_t hslot(uint32_t key, int64_t H) { return (key * 0x9E3779B1u) & (uint32_t)(H - 1); }
+
+// Floyd's collision test needs, for every drawn value, the first step that drew it: every
+// writer of a draw inserts (value -> min step) into the open-addressing table right away
+// (order-independent: CAS on the key, atomicMin on the step)
+__device__ __forceinline__ void rk_put(const RP& p, int64_t s, uint32_t v) {
+  p.w.draws[s] = v;
+  if (p.tail_shuffle) return;  // the tail shuffle keeps its own (position -> value) table
+  uint32_t h = hslot(v, p.w.H);
+  while (true) {
+    const uint32_t prev = atomicCAS(&p.w.htab[2 * h], 0xffffffffu, v);
+    if (prev == 0xffffffffu || prev == v) { atomicMin(&p.w.htab[2 * h + 1], (uint32_t)s); break; }
+    h = (h + 1) & (uint32_t)(p.w.H - 1);
+  }
 }
 
 // Lemire-32 rejection of numpy's bounded draw in [0, j] (random_bounded_uint64 ->
@@ -700,21 +719,6 @@ __device__ __forceinline__ uint64_t step_range(const RP& p, int64_t s) {
   return p.tail_shuffle ? (uint64_t)(p.n - 1 - s) : (uint64_t)(p.n - p.k + s);
 }
 
-// 32-bit draw stream precomputed in parallel (8 words per Philox block).
-__global__ void k_randk_words(RP p, uint32_t* words, int64_t nwords) {
-  const Philox ph = randk_philox(p);
-  for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 8 * blk < nwords;
-       blk += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t w[4];
-    ph.block(blk, w);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (8 * blk + 2 * q < nwords) words[8 * blk + 2 * q] = (uint32_t)w[q];
-      if (8 * blk + 2 * q + 1 < nwords) words[8 * blk + 2 * q + 1] = (uint32_t)(w[q] >> 32);
-    }
-  }
-}
-
 // One CTA walks the draw stream in windows of 1024 positions.  Step s consumes draws
 // until Lemire accepts for range j_s, so position q serves step q - t(q) with t the
 // rejections before q.  Per window every position evaluates 16 candidate offsets t0+d
@@ -724,8 +728,8 @@ __global__ void k_randk_words(RP p, uint32_t* words, int64_t nwords) {
 // whose offset would leave the 16 candidates (more rejections than candidates).
 constexpr int WD = 16;
 
-__global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words, int64_t nwords,
-                                                     const int64_t* start /* base, t0 or null */) {
+// (1024 threads; every thread of the CTA calls it)
+__device__ void randk_walk_body(const RP& p, const uint32_t* words, int64_t nwords, int64_t base0, int64_t t00) {
   __shared__ uint32_t smask[32][WD];
   __shared__ uint8_t sF[32][WD];
   __shared__ int s_enter[33];
@@ -733,8 +737,7 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
   __shared__ int64_t s_base, s_t0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Philox ph = randk_philox(p);
-  if (start && start[0] < 0) return;  // the multi-SM walk served every step
-  if (tid == 0) { s_base = start ? start[0] : 0; s_t0 = start ? start[1] : 0; }
+  if (tid == 0) { s_base = base0; s_t0 = t00; }
   __syncthreads();
   int64_t pf_pos = s_base + tid;  // prefetched word for the (likely) next window position
   uint32_t pf = pf_pos < nwords ? words[pf_pos] : draw32(ph, (uint64_t)pf_pos);
@@ -822,7 +825,7 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
           uint32_t v;
           const uint32_t w = q < nwords ? words[q] : draw32(ph, (uint64_t)q);
           if (lemire_reject(w, step_range(p, q - t) + 1, v)) ++t;
-          else p.w.draws[q - t] = v;
+          else rk_put(p, q - t, v);
         }
         s_base = q;
         s_t0 = t;
@@ -850,7 +853,7 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
       if (!((R >> lane) & 1u) && s >= 0 && s < p.k) {
         uint32_t v;
         lemire_reject(w32, step_range(p, s) + 1, v);
-        p.w.draws[s] = v;
+        rk_put(p, s, v);
       }
     }
     __syncthreads();
@@ -860,6 +863,10 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words, int64_t nwords) {
+  randk_walk_body(p, words, nwords, 0, 0);
 }
 
 // ---- multi-SM draw walk ------------------------------------------------------------------
@@ -930,10 +937,28 @@ __device__ void randk_drift(const RP& p, int64_t S, double& mean, double& var) {
   }
 }
 
+// Per-step scratch the later randk kernels need zeroed (bitmap, hash table, the emit's
+// look-back ticket + status, the link kernel's CTA counter): cleared by the tables kernel's
+// CTAs on their way, instead of three memset launches
+struct RkInit {
+  uint32_t* ts;  int64_t ts_words;  // ticket + status -> 0
+  uint32_t* bm;  int64_t bm_words;  // bitmap -> 0
+  uint32_t* ht;  int64_t ht_words;  // hash (key, step) -> 0xffffffff
+  uint32_t* done;                   // k_randk_link's finished-CTA counter -> 0
+};
+__device__ __forceinline__ void fill_words(uint32_t* d, int64_t nw, uint32_t v, int64_t i0, int64_t stride) {
+  // d is 16-byte aligned (carve); uint4 body, scalar tail
+  const int64_t n4 = nw >> 2;
+  for (int64_t i = i0; i < n4; i += stride) reinterpret_cast<uint4*>(d)[i] = make_uint4(v, v, v, v);
+  for (int64_t i = 4 * n4 + i0; i < nw; i += stride) d[i] = v;
+}
+
 constexpr int HQ = 16;  // queued filter hits per thread (mean ~3.2 at 1% density)
+// two 1024-thread CTAs per SM (<= 32 registers) when the smem allows it (DW = 512): the
+// ~270-window grid of a 25M-element group is then one wave, not two
 template <int DW, int RX>
-__global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int64_t nwin, int64_t* Lw,
-                               uint8_t* tables) {
+__global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, uint32_t* words, int64_t nwords, int64_t nwin, int64_t* Lw,
+                               uint8_t* tables, RkInit ini) {
   extern __shared__ uint32_t masks[];  // [DW + RX][32] then the hit queues [1024][HQ] u16
   uint16_t* hitq = reinterpret_cast<uint16_t*>(masks + (DW + RX) * 32);
   __shared__ int64_t s_L;
@@ -948,7 +973,7 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int6
     if (tid == 0) {
       double t, vv;
       randk_drift(p, w * WP, t, vv);
-      const int half = (int)ceil(6.0 * sqrt(vv)) + 16;
+      const int half = (int)ceil((double)p.band_sig * sqrt(vv)) + 16;
       const int dw = (int)imin(DW, (int64_t)((2 * half + 31) / 32 * 32));
       const int64_t L = imax(0, (int64_t)floor(t) - dw / 2);
       s_L = L;
@@ -961,7 +986,17 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int6
   const int dwin = s_dw;
   const Philox ph = randk_philox(p);
   const int64_t pos = w * WP + tid;
-  const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
+  // the draw word, generated here (8 threads share a Philox block; SIMT makes the redundancy
+  // free next to the filter) and kept for the emit's re-walk
+  const uint32_t w32 = draw32(ph, (uint64_t)pos);
+  if (pos < nwords) words[pos] = w32;
+  {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + tid, gs = (int64_t)gridDim.x * blockDim.x;
+    fill_words(ini.ts, ini.ts_words, 0u, gi, gs);
+    fill_words(ini.bm, ini.bm_words, 0u, gi, gs);
+    fill_words(ini.ht, ini.ht_words, 0xffffffffu, gi, gs);
+    if (gi == 0) *ini.done = 0u;
+  }
   for (int i = tid; i < (dwin + RX) * 32; i += blockDim.x) masks[i] = 0u;
   __syncthreads();
   // candidate c serves step s = pos - L - c: lo32(w * excl) moves by -+w and excl by -+1 per
@@ -1018,47 +1053,82 @@ __global__ void k_randk_tables(RP p, const uint32_t* words, int64_t nwords, int6
   }
 }
 
-// chain, in two levels: windows are grouped by CG; k_randk_compose turns each group's CG
-// tables into one composed table over the group's first window (thread e walks the
-// group from entering offset L + e), then k_randk_chain runs the serial recurrence over
-// groups (nwin / CG dependent lookups instead of nwin) and replays every group's windows
-// from its exact entering offset in parallel, writing tin[w].
+// chain, in two levels, one launch: windows are grouped by CG; CTA g composes its group's CG
+// tables (staged in shared memory) into one table over the group's first window — thread e
+// walks the group from entering offset L_g + e, recording every intermediate entering offset
+// mid[w][e] (-1 once the walk left the range) and the exit comp[g][e].  The last CTA to
+// finish (counter) runs the serial recurrence over groups on a shared-memory copy of comp
+// (ngrp dependent shared loads), replays every window's exact entering offset in parallel
+// (one mid lookup each -> tin[w]), and, if the chain ever left a window's speculated range,
+// walks the rest of the stream itself (randk_walk_body: slower, never wrong).
 constexpr int CG = 16;
-// compose also records every intermediate entering offset: mid[w][e] = the offset window w
-// is entered with when its group is entered at L_g + e (-1 once the walk left the range), so
-// the replay below is one lookup per window, all windows in parallel
+constexpr int64_t RK_LINK_SMEM = 160 * 1024;  // largest staged comp copy (+ static smem <= 227 KB)
 template <int DW>
-__global__ void __launch_bounds__(DW) k_randk_compose(const int64_t* Lw, const uint8_t* tables, int64_t nwin,
-                                                      int* comp, int* mid) {
-  const int64_t g = blockIdx.x, w0 = g * CG;
-  int t = (int)Lw[w0] + (int)threadIdx.x;
-  for (int64_t w = w0; w < imin(nwin, w0 + CG); ++w) {
-    mid[w * DW + threadIdx.x] = t;
-    if (t < 0) continue;
-    const unsigned c = (unsigned)(t - (int)Lw[w]);
-    const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
-    t = (r == 255) ? -1 : t + r;  // -1: left the speculated range inside the group
+__global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words, int64_t nwords, const int64_t* Lw,
+                                                     const uint8_t* tables, int64_t nwin, int* comp, int* mid, int* tg,
+                                                     int64_t* tin, WalkCtl* ctl, uint32_t* done, int stage_comp) {
+  __shared__ __align__(16) uint8_t s_tab[CG * DW];
+  __shared__ int s_L[CG];
+  __shared__ bool s_last;
+  extern __shared__ int s_dyn[];  // last CTA: group bases [ngrp] then comp as int16 relative to them
+  const int tid = threadIdx.x;
+  const int64_t ngrp = cdiv(nwin, CG);
+  {
+    const int64_t g = blockIdx.x, w0 = g * CG;
+    const int nwg = (int)imin(CG, nwin - w0);
+    const uint4* src4 = reinterpret_cast<const uint4*>(tables + w0 * DW);
+    for (int i = tid; i < nwg * DW / 16; i += blockDim.x) reinterpret_cast<uint4*>(s_tab)[i] = src4[i];
+    if (tid < nwg) s_L[tid] = (int)Lw[w0 + tid];
+    __syncthreads();
+    if (tid < DW) {
+      int t = s_L[0] + tid;
+      for (int w = 0; w < nwg; ++w) {
+        mid[(w0 + w) * DW + tid] = t;
+        if (t < 0) continue;
+        const unsigned c = (unsigned)(t - s_L[w]);
+        const int r = c < (unsigned)DW ? (int)s_tab[w * DW + c] : 255;
+        t = (r == 255) ? -1 : t + r;  // -1: left the speculated range inside the group
+      }
+      comp[g * DW + tid] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
   }
-  comp[g * DW + threadIdx.x] = t;
-}
-
-template <int DW>
-__global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, const uint8_t* tables, int64_t nwin,
-                                                      const int* comp, const int* mid, int* tg, int64_t* tin,
-                                                      WalkCtl* ctl) {
+  // ---- the last CTA: every group's comp / mid is written
   __shared__ int s_ng, s_texit;
   __shared__ unsigned long long s_served, s_fail;
-  __shared__ int s_Lg[1024];  // group entry bases (ngrp <= 1024 keeps the serial loop on smem)
-  const int64_t ngrp = cdiv(nwin, CG);
-  for (int64_t g = threadIdx.x; g < ngrp && g < 1024; g += blockDim.x) s_Lg[g] = (int)Lw[g * CG];
-  __syncthreads();
-  if (threadIdx.x == 0) {  // serial over groups: nwin / CG dependent lookups (one L2 load each)
+  __shared__ int64_t s_fb, s_ft0;
+  int* s_Lg = s_dyn;
+  int16_t* s_comp = reinterpret_cast<int16_t*>(s_dyn + ngrp);
+  if (stage_comp) {
+    for (int64_t g = tid; g < ngrp; g += blockDim.x) s_Lg[g] = (int)Lw[g * CG];
+    __syncthreads();
+    for (int64_t i = tid; i < ngrp * DW; i += blockDim.x) {
+      const int c = __ldcg(comp + i);
+      s_comp[i] = (int16_t)(c < 0 ? -1 : c - s_Lg[i / DW]);  // < DW + CG * RX: fits int16
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {  // serial over groups: ngrp dependent lookups
     int t = 0;
     int64_t g = 0;
     for (; g < ngrp; ++g) {
       tg[g] = t;
-      const unsigned c = (unsigned)(t - (g < 1024 ? s_Lg[g] : (int)Lw[g * CG]));
-      const int nt = c < (unsigned)DW ? comp[g * DW + c] : -1;
+      const int Lg = stage_comp ? s_Lg[g] : (int)Lw[g * CG];
+      const unsigned c = (unsigned)(t - Lg);
+      int nt = -1;
+      if (c < (unsigned)DW) {
+        if (stage_comp) {
+          const int r = s_comp[g * DW + c];
+          nt = r < 0 ? -1 : Lg + r;
+        } else {
+          nt = __ldcg(comp + g * DW + c);
+        }
+      }
       if (nt < 0) { ++g; break; }  // the failure lies inside this group: found below
       t = nt;
     }
@@ -1070,12 +1140,12 @@ __global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, c
   // every window of those groups in parallel: its entering offset, the first window whose
   // steps are all served (nwin_used) and the first that leaves its range (serial hand-over)
   const int64_t nw = imin(nwin, (int64_t)s_ng * CG);
-  for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) {
+  for (int64_t w = tid; w < nw; w += blockDim.x) {
     const int64_t g = w / CG, w0 = g * CG;
     const unsigned e = (unsigned)(tg[g] - (int)Lw[w0]);
     int t;
     if (e < (unsigned)DW) {
-      t = mid[w * DW + e];
+      t = __ldcg(mid + w * DW + e);
       if (t < 0) continue;  // past this group's failing window
     } else {
       if (w != w0) continue;  // the group is entered outside its range: fails at its first window
@@ -1086,29 +1156,33 @@ __global__ void __launch_bounds__(1024) k_randk_chain(RP p, const int64_t* Lw, c
     const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
     if (r == 255) {  // at most one such window: the chain's first failure
       atomicMin(&s_fail, (unsigned long long)w);
-      ctl->fail_t0 = t;
+      s_ft0 = t;
       continue;
     }
     tin[w] = t;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    ctl->fail_base = -1;
+  if (tid == 0) {
+    s_fb = -1;
     if (s_fail < s_served) {
-      ctl->fail_base = (int64_t)s_fail * WP;
+      s_fb = (int64_t)s_fail * WP;
       ctl->nwin_used = (int64_t)s_fail;
     } else {
       ctl->nwin_used = (int64_t)s_served;
       if (s_served == (unsigned long long)nwin && nwin * WP - (int64_t)s_texit < p.k) {
-        ctl->fail_base = nwin * WP;  // ran out of windows before every step was served
-        ctl->fail_t0 = s_texit;
+        s_fb = nwin * WP;  // ran out of windows before every step was served
+        s_ft0 = s_texit;
       }
     }
+    ctl->fail_base = s_fb;
+    ctl->fail_t0 = s_ft0;
   }
+  __syncthreads();
+  if (s_fb >= 0) randk_walk_body(p, words, nwords, s_fb, s_ft0);  // > 6 sd excursion (rare)
 }
 
 template <int RX>
-__global__ void __launch_bounds__(1024) k_randk_emit_draws(RP p, const uint32_t* words, int64_t nwords,
+__global__ void __launch_bounds__(1024, 2) k_randk_emit_draws(RP p, const uint32_t* words, int64_t nwords,
                                                            const int64_t* tin, const WalkCtl* ctl) {
   __shared__ uint32_t smask[RX][32];
   __shared__ int s_enter[32];
@@ -1116,12 +1190,29 @@ __global__ void __launch_bounds__(1024) k_randk_emit_draws(RP p, const uint32_t*
   if (w >= ctl->nwin_used) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t0 = tin[w];
-  const Philox ph = randk_philox(p);
   const int64_t pos = w * WP + tid;
-  const uint32_t w32 = pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos);
-  for (int d = 0; d < RX; ++d) {
-    const unsigned m = __ballot_sync(FULL, rejects(p, w32, pos - t0 - d));
-    if (lane == 0) smask[d][warp] = m;
+  const uint32_t w32 = words[pos];  // written by the tables kernel for every window position
+  for (int i = tid; i < RX * 32; i += blockDim.x) (&smask[0][0])[i] = 0u;
+  __syncthreads();
+  {  // rejection masks of offsets t0 + d: the tables kernel's two-op filter, exact test on hits
+    const int64_t s0 = pos - t0;
+    const uint32_t ex0 = excl_of(p, s0);
+    const uint32_t dl = p.tail_shuffle ? w32 : (0u - w32);
+    const uint32_t exb = p.tail_shuffle ? ex0 + (uint32_t)RX : ex0;
+    uint32_t left = w32 * ex0;
+    for (int c0 = 0; c0 < RX; c0 += 32) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        m |= left < exb ? (1u << j) : 0u;
+        left += dl;
+      }
+      while (m) {
+        const int d = c0 + __ffs(m) - 1;
+        m &= m - 1;
+        if (rejects(p, w32, s0 - d)) atomicOr(&smask[d][warp], 1u << lane);
+      }
+    }
   }
   __syncthreads();
   if (tid == 0) {  // entering offsets of the 32 warps along the true path (<= RX-1 rejections)
@@ -1156,21 +1247,7 @@ __global__ void __launch_bounds__(1024) k_randk_emit_draws(RP p, const uint32_t*
   if (!((R >> lane) & 1u) && s >= 0 && s < p.k) {
     uint32_t v;
     lemire_reject(w32, (uint64_t)excl_of(p, s), v);
-    p.w.draws[s] = v;
-  }
-}
-
-__device__ __forceinline__ uint32_t hslot(uint32_t key, int64_t H) { return (key * 0x9E3779B1u) & (uint32_t)(H - 1); }
-
-__global__ void k_randk_insert(RP p) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < p.k; s += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t key = p.w.draws[s];
-    uint32_t h = hslot(key, p.w.H);
-    while (true) {
-      const uint32_t prev = atomicCAS(&p.w.htab[2 * h], 0xffffffffu, key);
-      if (prev == 0xffffffffu || prev == key) { atomicMin(&p.w.htab[2 * h + 1], (uint32_t)s); break; }
-      h = (h + 1) & (uint32_t)(p.w.H - 1);
-    }
+    rk_put(p, s, v);
   }
 }
 
@@ -1656,6 +1733,10 @@ int encode_randk(const EncodeArgs& a, float* out) {
   p.unbiased = a.spec->unbiased_scaling;
   p.scale = (float)((double)n / (double)k);  // np.float32(n / k)  (compressors.py:284)
   p.tail_shuffle = (n > 10000 && k > n / 50) ? 1 : 0;
+  {  // MC_RANDK_BAND_SIGMA: test knob (a narrow band forces the serial fallback; results never change)
+    const char* e = getenv("MC_RANDK_BAND_SIGMA");
+    p.band_sig = e ? (float)atof(e) : 6.0f;
+  }
   p.out = out;
   p.payload = a.payload;
   p.hdr.algorithm = MC_RANDK;
@@ -1665,24 +1746,30 @@ int encode_randk(const EncodeArgs& a, float* out) {
   cudaStream_t st = a.ctx.stream;
   const int64_t nwords = cdiv(n, 32);
   const int64_t nblk = cdiv(nwords, TB * 4) + 1;
-  MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st));
-  MC_API_CHECK(cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st));
-  MC_API_CHECK(cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st));
+  const bool vec = (uintptr_t)p.pro.g % 16 == 0 && (!out || (uintptr_t)out % 16 == 0) &&
+                   (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) && (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0);
+  auto memsets = [&]() -> int {
+    MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (nblk + 1), st));
+    MC_API_CHECK(cudaMemsetAsync(p.w.bitmap, 0, 4 * nwords, st));
+    MC_API_CHECK(cudaMemsetAsync(p.w.htab, 0xff, 8 * p.w.H, st));
+    return MC_OK;
+  };
   if (k == n) {
+    if (int rc = memsets()) return rc;
     note_launch(); k_bitmap_all<<<(unsigned)imax(1, imin(cdiv(nwords, 256), 1024)), 256, 0, st>>>(p);
   } else {
     // the 32-bit draw stream (k + margin for rejections) in the unused candidate-list area;
-    // walk scratch after it: expectations, L_w, entering offsets, tables, control
-    const int64_t nwords = imin(n, k + k / 16 + 4096);
-    const int64_t nwin = cdiv(nwords, WP);
-    uint8_t* wsb = reinterpret_cast<uint8_t*>(p.w.list) + a16(4 * nwords);
-    // wsb[0, 16 nwin): spare (the per-window drift sums are closed forms now, randk_drift)
+    // walk scratch after it: L_w, entering offsets, control, tables, composed tables
+    const int64_t ndraw = imin(n, k + k / 16 + 4096);
+    const int64_t nwin = cdiv(ndraw, WP);
+    const int64_t nwpos = nwin * WP;  // draw words kept for every window position
+    uint8_t* wsb = reinterpret_cast<uint8_t*>(p.w.list) + a16(4 * nwpos);
     int64_t* Lw = reinterpret_cast<int64_t*>(wsb + a16(16 * nwin));
     int64_t* tin = reinterpret_cast<int64_t*>(wsb + a16(16 * nwin) + a16(8 * nwin));
     WalkCtl* ctl = reinterpret_cast<WalkCtl*>(wsb + a16(16 * nwin) + 2 * a16(8 * nwin));
     uint8_t* tables = wsb + a16(16 * nwin) + 2 * a16(8 * nwin) + 64;
-    // exact drift statistics of this (n, k) stream, once per group shape: sd of the total
-    // rejections and the largest mean rejection count of a 1024-draw window
+    // exact drift statistics of this (n, k) stream: sd of the total rejections and the largest
+    // mean rejection count of a 1024-draw window
     const RandkStats rs = randk_stats(n, k, p.tail_shuffle != 0);
     const int DWr = rs.sd > 100.0 ? 1024 : 512;  // +-256 covers >= 2.56 sd; the rest falls back
     const double mu = rs.window_mean_max;
@@ -1693,22 +1780,28 @@ int encode_randk(const EncodeArgs& a, float* out) {
       return sum * (double)nwin;
     };
     const int RXr = tail(32) < 1e-6 ? 32 : tail(64) < 1e-6 ? 64 : 96;
-    int* comp = reinterpret_cast<int*>(tables + a16(nwin * DWr));           // [ngroups][DW]
-    int* tg = comp + cdiv(nwin, CG) * DWr;                                   // [ngroups]
-    int* mid = tg + cdiv(nwin, CG) + 4;                                      // [nwin][DW]
-    note_launch(); k_randk_words<<<(unsigned)imax(1, imin(cdiv(nwords, 8 * 256), (int64_t)sm_count() * 4)), 256, 0, st>>>(p, p.w.list, nwords);
-    if (4 * n >= a16(4 * nwords) + a16(16 * nwin) + 2 * a16(8 * nwin) + 64 + a16(nwin * DWr) +
-                     4 * (cdiv(nwin, CG) * (DWr + 1) + 4 + nwin * DWr)) {  // room for the parallel walk
-      const int64_t ngrp = cdiv(nwin, CG);
-#define MC_RANDK_WALK(DWV, RXV)                                                                                    \
-  {                                                                                                               \
-    const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2;                                                          \
-    static std::atomic<uint64_t> cfg{0}; /* per device */                                                         \
-    MC_API_CHECK(smem_optin(cfg, k_randk_tables<DWV, RXV>, ts));                                                  \
-    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwords, nwin, Lw, tables); \
-    note_launch(); k_randk_compose<DWV><<<(unsigned)ngrp, DWV, 0, st>>>(Lw, tables, nwin, comp, mid);                 \
-    note_launch(); k_randk_chain<DWV><<<1, 1024, 0, st>>>(p, Lw, tables, nwin, comp, mid, tg, tin, ctl);              \
-    note_launch(); k_randk_emit_draws<RXV><<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwords, tin, ctl);           \
+    const int64_t ngrp = cdiv(nwin, CG);
+    int* comp = reinterpret_cast<int*>(tables + a16(nwin * DWr));  // [ngroups][DW]
+    int* tg = comp + ngrp * DWr;                                    // [ngroups]
+    int* mid = tg + ngrp + 4;                                       // [nwin][DW]
+    if (4 * n >= a16(4 * nwpos) + a16(16 * nwin) + 2 * a16(8 * nwin) + 64 + a16(nwin * DWr) +
+                     4 * (ngrp * (DWr + 1) + 4 + nwin * DWr)) {  // room for the parallel walk
+      // 4 launches to the bitmap: tables (+ scratch init + draw words), link (compose + chain +
+      // rare serial fallback), emit_draws (+ hash insert), floyd_mark / tail shuffle
+      RkInit ini{p.w.ticket, (16 + 8 * (nblk + 1)) / 4, p.w.bitmap, nwords, p.w.htab, 2 * p.w.H, p.w.ctl};
+      const int64_t link_smem = 4 * ngrp + 2 * ngrp * DWr;
+      const int stage_comp = link_smem <= RK_LINK_SMEM;
+#define MC_RANDK_WALK(DWV, RXV)                                                                                        \
+  {                                                                                                                   \
+    const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2;                                                              \
+    static std::atomic<uint64_t> cfg{0}, cfgl{0}; /* per device */                                                    \
+    MC_API_CHECK(smem_optin(cfg, k_randk_tables<DWV, RXV>, ts));                                                      \
+    note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwpos, nwin, Lw, tables, ini); \
+    const int ls = stage_comp ? (int)a16(link_smem) : 0;                                                              \
+    MC_API_CHECK(smem_optin(cfgl, k_randk_link<DWV>, (int)a16(RK_LINK_SMEM)));                                         \
+    note_launch(); k_randk_link<DWV><<<(unsigned)ngrp, 1024, ls, st>>>(p, p.w.list, nwpos, Lw, tables, nwin, comp, mid,  \
+                                                                        tg, tin, ctl, p.w.ctl, stage_comp);           \
+    note_launch(); k_randk_emit_draws<RXV><<<(unsigned)nwin, 1024, 0, st>>>(p, p.w.list, nwpos, tin, ctl);            \
   }
       if (DWr == 512 && RXr == 32) MC_RANDK_WALK(512, 32)
       else if (DWr == 512 && RXr == 64) MC_RANDK_WALK(512, 64)
@@ -1717,20 +1810,17 @@ int encode_randk(const EncodeArgs& a, float* out) {
       else if (RXr == 64) MC_RANDK_WALK(1024, 64)
       else MC_RANDK_WALK(1024, 96)
 #undef MC_RANDK_WALK
-      note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, &ctl->fail_base);
     } else {
-      note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, nwords, nullptr);
+      if (int rc = memsets()) return rc;
+      note_launch(); k_randk_walk<<<1, 1024, 0, st>>>(p, p.w.list, 0);  // words generated on the fly
     }
     if (p.tail_shuffle) {
       note_launch(); k_randk_tail_shuffle<<<1, 1, 0, st>>>(p);
     } else {
       const unsigned gk = (unsigned)imax(1, imin(cdiv(k, 256), (int64_t)sm_count() * 8));
-      note_launch(); k_randk_insert<<<gk, 256, 0, st>>>(p);
       note_launch(); k_randk_floyd_mark<<<gk, 256, 0, st>>>(p);
     }
   }
-  const bool vec = (uintptr_t)p.pro.g % 16 == 0 && (!out || (uintptr_t)out % 16 == 0) &&
-                   (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) && (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0);
   const unsigned ge = (unsigned)cdiv(nwords, TB * 4);
   note_launch();
 #define MC_RK_EMIT(EF, MOM)                                                 \

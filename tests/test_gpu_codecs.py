@@ -127,6 +127,28 @@ def test_derive_seed_native_matches_table(C):
         assert C.derive_seed(root, w, t, g) == (lo | (hi << 64))
 
 
+@pytest.mark.parametrize("sigma", ["0", "1.5"])
+def test_randk_serial_fallback_matches_oracle(sigma, C, monkeypatch):
+    """A speculated-offset band too narrow for the walk's drift (MC_RANDK_BAND_SIGMA, a test
+    knob) makes the chain leave a window's range: the link kernel's last CTA then walks the rest
+    of the stream serially.  Results must not change (bit-exact vs the oracle)."""
+    import torch
+
+    import mergecomp_oracle as O
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    monkeypatch.setenv("MC_RANDK_BAND_SIGMA", sigma)
+    n = 4_000_037
+    spec = CompressorSpec("randk", sparsity=0.99)
+    g = (np.random.default_rng(5).standard_normal(n) * 1e-3).astype(np.float32)
+    seed = O.derive_seed(11, 1, 2, 0)
+    p_dev, _ = C.encode(spec, torch.from_numpy(g).cuda(), None, seed=seed)
+    p_ref, _ = O.encode(spec, g, None, seed=seed)
+    d = p_dev.to_host()
+    assert np.array_equal(np.asarray(d.indices), np.asarray(p_ref.indices))
+    assert np.array_equal(np.asarray(d.values).view(np.uint32), np.asarray(p_ref.values).view(np.uint32))
+
+
 @pytest.mark.parametrize("n,sparsity", [(2_000_003, 0.99), (3_000_000, 0.995), (1_500_000, 0.9)])
 def test_randk_multi_window_walk_matches_oracle(n, sparsity, C):
     """randk at sizes where the draw walk spans many 1024-position windows (speculative

@@ -20,6 +20,9 @@ SPECS = [
     dict(algorithm="dgc_lite", sparsity=0.99),
     dict(algorithm="topk", sparsity=0.9),
     dict(algorithm="randk", sparsity=0.99),
+    dict(algorithm="randk", sparsity=0.99, error_feedback=True, momentum=0.9, unbiased_scaling=True),
+    dict(algorithm="randk", sparsity=0.95, error_feedback=True),
+    dict(algorithm="randk", sparsity=0.99, momentum=0.5),
     dict(algorithm="threshold", threshold=2e-3),
     dict(algorithm="signsgd"),
     dict(algorithm="signum"),
