@@ -953,14 +953,31 @@ __device__ __forceinline__ void fill_words(uint32_t* d, int64_t nw, uint32_t v, 
   for (int64_t i = 4 * n4 + i0; i < nw; i += stride) d[i] = v;
 }
 
+// 32 consecutive candidates' filter bits in three instructions each: left + (2^32 - exb)
+// carries out exactly when left >= exb (no hit), and madc shifts that carry into the mask
+// (m = 2 m + carry) — one integer-ALU op per candidate where compare + select + merge took
+// three; the mask comes out MSB-first and inverted, hence the final brev / not.
+// Returns bit j = (left_j < exb) for left_j = left + j dl; advances left by 32 dl.
+__device__ __forceinline__ uint32_t filter32(uint32_t& left, uint32_t dl, uint32_t exb) {
+  const uint32_t K = 0u - exb;
+  uint32_t m = 0, t;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    asm("add.cc.u32 %0, %2, %3;\n\tmadc.lo.u32 %1, %1, 2, 0;" : "=r"(t), "+r"(m) : "r"(left), "r"(K));
+    left += dl;
+  }
+  return ~__brev(m);
+}
+
 constexpr int HQ = 16;  // queued filter hits per thread (mean ~3.2 at 1% density)
 // two 1024-thread CTAs per SM (<= 32 registers) when the smem allows it (DW = 512): the
 // ~270-window grid of a 25M-element group is then one wave, not two
 template <int DW, int RX>
 __global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, uint32_t* words, int64_t nwords, int64_t nwin, int64_t* Lw,
                                uint8_t* tables, RkInit ini) {
-  extern __shared__ uint32_t masks[];  // [DW + RX][32] then the hit queues [1024][HQ] u16
+  extern __shared__ uint32_t masks[];  // [DW + RX][32], the hit queues [1024][HQ] u16, row summaries [DW + RX]
   uint16_t* hitq = reinterpret_cast<uint16_t*>(masks + (DW + RX) * 32);
+  uint32_t* rownz = reinterpret_cast<uint32_t*>(hitq + 1024 * HQ);  // bit j: row c has a rejection in word j
   __shared__ int64_t s_L;
   __shared__ int s_dw;
   const int64_t w = blockIdx.x;
@@ -998,6 +1015,7 @@ __global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, 
     if (gi == 0) *ini.done = 0u;
   }
   for (int i = tid; i < (dwin + RX) * 32; i += blockDim.x) masks[i] = 0u;
+  for (int i = tid; i < dwin + RX; i += blockDim.x) rownz[i] = 0u;
   __syncthreads();
   // candidate c serves step s = pos - L - c: lo32(w * excl) moves by -+w and excl by -+1 per
   // candidate, so the "may reject" filter (left < excl, p ~ excl / 2^32 < 1%) is two adds and a
@@ -1017,34 +1035,43 @@ __global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, 
   uint16_t* q = hitq + tid * HQ;
   int nh = 0;
   for (int c0 = 0; c0 < nc; c0 += 32) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      m |= left < exb ? (1u << j) : 0u;
-      left += dl;
-    }
+    uint32_t m = filter32(left, dl, exb);
     if (nc - c0 < 32) m &= (1u << (nc - c0)) - 1u;
     while (m) {
       const int c = c0 + __ffs(m) - 1;
       m &= m - 1;
       if (nh < HQ) q[nh++] = (uint16_t)c;
-      else if (rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);  // (never in practice)
+      else if (rejects(p, w32, s0 - c)) {  // (never in practice)
+        atomicOr(&masks[c * 32 + warp], 1u << lane);
+        atomicOr(&rownz[c], 1u << warp);
+      }
     }
   }
   const int nmax = __reduce_max_sync(FULL, nh);
   for (int i = 0; i < nmax; ++i) {
     const int c = i < nh ? q[i] : 0;
-    if (i < nh && rejects(p, w32, s0 - c)) atomicOr(&masks[c * 32 + warp], 1u << lane);
+    if (i < nh && rejects(p, w32, s0 - c)) {
+      atomicOr(&masks[c * 32 + warp], 1u << lane);
+      atomicOr(&rownz[c], 1u << warp);
+    }
   }
   __syncthreads();
   if (tid < dwin) {  // walk entering with offset L + tid
+    // the row summaries jump straight to the next mask word holding a rejection: a few shared
+    // loads per rejection instead of a scan of all 32 words of every row on the path
     int d = tid, bit = 0;
     bool ok = true;
     while (bit < WP) {
       const int word = bit >> 5;
-      const uint32_t m = masks[d * 32 + word] & (0xffffffffu << (bit & 31));
-      if (!m) { bit = (word + 1) * 32; continue; }
-      bit = word * 32 + __ffs(m);  // position after the rejection
+      uint32_t m = masks[d * 32 + word] & (0xffffffffu << (bit & 31));
+      int wb = word;
+      if (!m) {
+        const uint32_t nz = word < 31 ? rownz[d] & (0xfffffffeu << word) : 0u;  // words after `word`
+        if (!nz) break;  // no rejection left on row d: the walk stays on it to the window's end
+        wb = __ffs(nz) - 1;
+        m = masks[d * 32 + wb];
+      }
+      bit = wb * 32 + __ffs(m);  // position after the rejection
       if (++d >= dwin + RX || d - tid >= RX) { ok = false; break; }
     }
     tables[w * DW + tid] = ok ? (uint8_t)(d - tid) : (uint8_t)255;
@@ -1201,12 +1228,7 @@ __global__ void __launch_bounds__(1024, 2) k_randk_emit_draws(RP p, const uint32
     const uint32_t exb = p.tail_shuffle ? ex0 + (uint32_t)RX : ex0;
     uint32_t left = w32 * ex0;
     for (int c0 = 0; c0 < RX; c0 += 32) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        m |= left < exb ? (1u << j) : 0u;
-        left += dl;
-      }
+      uint32_t m = filter32(left, dl, exb);
       while (m) {
         const int d = c0 + __ffs(m) - 1;
         m &= m - 1;
@@ -1793,7 +1815,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
       const int stage_comp = link_smem <= RK_LINK_SMEM;
 #define MC_RANDK_WALK(DWV, RXV)                                                                                        \
   {                                                                                                                   \
-    const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2;                                                              \
+    const int ts = (DWV + RXV) * 32 * 4 + 1024 * HQ * 2 + (DWV + RXV) * 4;                                            \
     static std::atomic<uint64_t> cfg{0}, cfgl{0}; /* per device */                                                    \
     MC_API_CHECK(smem_optin(cfg, k_randk_tables<DWV, RXV>, ts));                                                      \
     note_launch(); k_randk_tables<DWV, RXV><<<(unsigned)nwin, 1024, ts, st>>>(p, p.w.list, nwpos, nwin, Lw, tables, ini); \
