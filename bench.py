@@ -53,6 +53,12 @@ def parse():
                          "and sparse codecs; allreduce_dense: the uncompressed fp32 NCCL all_reduce + /N "
                          "baseline of BASELINE config 5 (codec ignored)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--step-mode", default="auto", choices=["auto", "graph", "eager"],
+                    help="graph: time CUDA Graph replays of the pinned step (GradSync.capture_graph: one rank, or "
+                         "the peer exchange) after the eager pass that feeds the roofline probes; auto = graph "
+                         "where the step is capturable, else eager")
+    ap.add_argument("--graph", action="store_const", const="graph", dest="step_mode", help="= --step-mode graph")
+    ap.add_argument("--eager", action="store_const", const="eager", dest="step_mode", help="= --step-mode eager")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU oracle sample budget")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
@@ -424,6 +430,35 @@ def main():
     torch.cuda.synchronize()
     sync.check()
     ms_step = ms / args.steps
+    step_mode = "eager (one C-ABI call per group per step)"
+    capturable = sync.world == 1 or getattr(sync, "_peer", None) is not None
+    if args.step_mode == "graph" or (args.step_mode == "auto" and capturable):
+        # the same step as one CUDA Graph replay: the same kernels (launches counted in the eager
+        # pass above), no per-launch host gaps; inputs still the previous step's output (in place)
+        sync.probe = None
+        sync.capture_graph()
+        for _ in range(max(args.warmup, 3)):
+            sync.step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        sampler = ClockSampler(local)  # the clocks reported are those of the graph-timed region
+        with sampler:
+            start.record(sync.stream)
+            for _ in range(args.steps):
+                sync.step()
+            stop.record(sync.stream)
+            torch.cuda.synchronize()
+        ms = start.elapsed_time(stop)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        sync.check()
+        sync.drop_graph()
+        ms_step = ms / args.steps
+        step_mode = "CUDA Graph replay of the pinned step"
     value = world * 4.0 * D / (ms_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (EF bucket encode of the largest group)
@@ -504,6 +539,7 @@ def main():
                 "exchange": exchange_used,
                 "l2": "inputs larger than L2 (grads 4D + fp64 residual 8D bytes per rank, >> 126 MB)",
                 "input": "step t+1 encodes the averaged gradient written by step t (in place)",
+                "step_mode": step_mode,
             },
             "roofline": {
                 "bound": "hbm",
@@ -517,6 +553,8 @@ def main():
                 "kernel_ms": kern_ms,
                 "kernel_share_of_step": None if kern_ms is None else kern_ms / ms_step,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
+                "kernel_timing": "CUDA events around the kernel on the sync stream in the eager pass (the event "
+                                 "records add ~2-3 us); in graph mode the replayed step bounds the kernel from above",
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * D, "d2h_bytes_per_step": 4 * D,
