@@ -1097,7 +1097,7 @@ __global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words
   __shared__ __align__(16) uint8_t s_tab[CG * DW];
   __shared__ int s_L[CG];
   __shared__ bool s_last;
-  extern __shared__ int s_dyn[];  // last CTA: group bases [ngrp] then comp as int16 relative to them
+  extern __shared__ int s_dyn[];  // last CTA: group bases [ngrp], group entries [ngrp], comp as int16 relative
   const int tid = threadIdx.x;
   const int64_t ngrp = cdiv(nwin, CG);
   {
@@ -1130,13 +1130,24 @@ __global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words
   __shared__ unsigned long long s_served, s_fail;
   __shared__ int64_t s_fb, s_ft0;
   int* s_Lg = s_dyn;
-  int16_t* s_comp = reinterpret_cast<int16_t*>(s_dyn + ngrp);
+  int* s_tg = s_dyn + ngrp;
+  int16_t* s_comp = reinterpret_cast<int16_t*>(s_dyn + 2 * ngrp);
   if (stage_comp) {
     for (int64_t g = tid; g < ngrp; g += blockDim.x) s_Lg[g] = (int)Lw[g * CG];
     __syncthreads();
-    for (int64_t i = tid; i < ngrp * DW; i += blockDim.x) {
-      const int c = __ldcg(comp + i);
-      s_comp[i] = (int16_t)(c < 0 ? -1 : c - s_Lg[i / DW]);  // < DW + CG * RX: fits int16
+    // four independent L2 loads in flight per thread
+    for (int64_t i0 = tid; i0 < ngrp * DW; i0 += 4 * (int64_t)blockDim.x) {
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * (int64_t)blockDim.x;
+        c[u] = i < ngrp * DW ? __ldcg(comp + i) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * (int64_t)blockDim.x;
+        if (i < ngrp * DW) s_comp[i] = (int16_t)(c[u] < 0 ? -1 : c[u] - s_Lg[i / DW]);  // < DW + CG RX: int16
+      }
     }
     __syncthreads();
   }
@@ -1144,7 +1155,8 @@ __global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words
     int t = 0;
     int64_t g = 0;
     for (; g < ngrp; ++g) {
-      tg[g] = t;
+      if (stage_comp) s_tg[g] = t;
+      else tg[g] = t;
       const int Lg = stage_comp ? s_Lg[g] : (int)Lw[g * CG];
       const unsigned c = (unsigned)(t - Lg);
       int nt = -1;
@@ -1169,14 +1181,15 @@ __global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words
   const int64_t nw = imin(nwin, (int64_t)s_ng * CG);
   for (int64_t w = tid; w < nw; w += blockDim.x) {
     const int64_t g = w / CG, w0 = g * CG;
-    const unsigned e = (unsigned)(tg[g] - (int)Lw[w0]);
+    const int tgg = stage_comp ? s_tg[g] : tg[g];
+    const unsigned e = (unsigned)(tgg - (stage_comp ? s_Lg[g] : (int)Lw[w0]));
     int t;
     if (e < (unsigned)DW) {
       t = __ldcg(mid + w * DW + e);
       if (t < 0) continue;  // past this group's failing window
     } else {
       if (w != w0) continue;  // the group is entered outside its range: fails at its first window
-      t = tg[g];
+      t = tgg;
     }
     if (w * WP - (int64_t)t >= p.k) { atomicMin(&s_served, (unsigned long long)w); continue; }
     const unsigned c = (unsigned)(t - (int)Lw[w]);
@@ -1347,7 +1360,7 @@ __global__ void k_bitmap_all(RP p) {
 // published, so nobody waits; the pairs then go out as coalesced rows.  A CTA selecting more
 // than RK_STAGE elements (dense randk) resolves first and writes them from the bitmap before
 // streaming (its values must be read before the pass overwrites the state).
-constexpr int RK_STAGE = 4096;
+constexpr int RK_STAGE = 2048;  // 1% randk stages ~330 per CTA; denser CTAs write from the bitmap
 template <bool EF, bool MOM, bool VEC>
 __device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uint32_t* s_words, const uint32_t* s_rank,
                                           uint16_t* s_off, float* s_val, bool stage, bool& bad) {
@@ -1811,7 +1824,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
       // 4 launches to the bitmap: tables (+ scratch init + draw words), link (compose + chain +
       // rare serial fallback), emit_draws (+ hash insert), floyd_mark / tail shuffle
       RkInit ini{p.w.ticket, (16 + 8 * (nblk + 1)) / 4, p.w.bitmap, nwords, p.w.htab, 2 * p.w.H, p.w.ctl};
-      const int64_t link_smem = 4 * ngrp + 2 * ngrp * DWr;
+      const int64_t link_smem = 8 * ngrp + 2 * ngrp * DWr;
       const int stage_comp = link_smem <= RK_LINK_SMEM;
 #define MC_RANDK_WALK(DWV, RXV)                                                                                        \
   {                                                                                                                   \
