@@ -982,31 +982,35 @@ __global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, 
   __shared__ int s_dw;
   const int64_t w = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {  // expected offset at the window start and its variance (closed form; they only centre
-     // and size the speculated range — the chain checks it).  The range is +-(6 sd + 16), at
-     // most DW: early windows, whose offset is still nearly deterministic, evaluate a few
-     // dozen entering offsets instead of DW.  A > 6 sd excursion (p ~ 2e-9 per window) hands
-     // the rest of the stream to the serial walker: slower, never wrong
-    if (tid == 0) {
-      double t, vv;
-      randk_drift(p, w * WP, t, vv);
-      const int half = (int)ceil((double)p.band_sig * sqrt(vv)) + 16;
-      const int dw = (int)imin(DW, (int64_t)((2 * half + 31) / 32 * 32));
-      const int64_t L = imax(0, (int64_t)floor(t) - dw / 2);
-      s_L = L;
-      s_dw = dw;
-      Lw[w] = L;
-    }
-  }
-  __syncthreads();
-  const int64_t L = s_L;
-  const int dwin = s_dw;
+  __shared__ __align__(16) uint32_t s_w32[WP];
   const Philox ph = randk_philox(p);
-  const int64_t pos = w * WP + tid;
-  // the draw word, generated here (8 threads share a Philox block; SIMT makes the redundancy
-  // free next to the filter) and kept for the emit's re-walk
-  const uint32_t w32 = draw32(ph, (uint64_t)pos);
-  if (pos < nwords) words[pos] = w32;
+  if (tid == 128) {
+    // expected offset at the window start and its variance (closed form; they only centre and
+    // size the speculated range — the chain checks it).  The range is +-(6 sd + 16), at most
+    // DW: early windows, whose offset is still nearly deterministic, evaluate a few dozen
+    // entering offsets instead of DW.  A > 6 sd excursion (p ~ 2e-9 per window) hands the rest
+    // of the stream to the serial walker: slower, never wrong.  (Warp 4 computes this while
+    // warps 0-3 generate the window's draw words.)
+    double t, vv;
+    randk_drift(p, w * WP, t, vv);
+    const int half = (int)ceil((double)p.band_sig * sqrt(vv)) + 16;
+    const int dw = (int)imin(DW, (int64_t)((2 * half + 31) / 32 * 32));
+    const int64_t L = imax(0, (int64_t)floor(t) - dw / 2);
+    s_L = L;
+    s_dw = dw;
+    Lw[w] = L;
+  }
+  if (tid < WP / 8) {  // the window's 1024 draw words: 128 Philox blocks, one per thread of warps 0-3
+    uint64_t b[4];
+    ph.block((uint64_t)(w * (WP / 8) + tid), b);
+    const uint4 lo = make_uint4((uint32_t)b[0], (uint32_t)(b[0] >> 32), (uint32_t)b[1], (uint32_t)(b[1] >> 32));
+    const uint4 hi = make_uint4((uint32_t)b[2], (uint32_t)(b[2] >> 32), (uint32_t)b[3], (uint32_t)(b[3] >> 32));
+    reinterpret_cast<uint4*>(s_w32)[2 * tid] = lo;
+    reinterpret_cast<uint4*>(s_w32)[2 * tid + 1] = hi;
+    // kept for the emit's re-walk (nwords = every window position)
+    reinterpret_cast<uint4*>(words + w * WP)[2 * tid] = lo;
+    reinterpret_cast<uint4*>(words + w * WP)[2 * tid + 1] = hi;
+  }
   {
     const int64_t gi = (int64_t)blockIdx.x * blockDim.x + tid, gs = (int64_t)gridDim.x * blockDim.x;
     fill_words(ini.ts, ini.ts_words, 0u, gi, gs);
@@ -1014,6 +1018,11 @@ __global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, 
     fill_words(ini.ht, ini.ht_words, 0xffffffffu, gi, gs);
     if (gi == 0) *ini.done = 0u;
   }
+  __syncthreads();
+  const int64_t L = s_L;
+  const int dwin = s_dw;
+  const int64_t pos = w * WP + tid;
+  const uint32_t w32 = s_w32[tid];
   for (int i = tid; i < (dwin + RX) * 32; i += blockDim.x) masks[i] = 0u;
   for (int i = tid; i < dwin + RX; i += blockDim.x) rownz[i] = 0u;
   __syncthreads();
