@@ -1823,7 +1823,9 @@ int encode_randk(const EncodeArgs& a, float* out) {
       for (int j = r; j < r + 400 && term > 1e-300; ++j) { sum += term; term *= mu / (j + 1); }
       return sum * (double)nwin;
     };
-    const int RXr = tail(32) < 1e-6 ? 32 : tail(64) < 1e-6 ? 64 : 96;
+    // a window with more rejections than RX fails over to the serial walker (never wrong, ~ms):
+    // allowed with probability 1e-4 per step (~0.3 us of expected cost), not 1e-6
+    const int RXr = tail(32) < 1e-4 ? 32 : tail(64) < 1e-4 ? 64 : 96;
     const int64_t ngrp = cdiv(nwin, CG);
     int* comp = reinterpret_cast<int*>(tables + a16(nwin * DWr));  // [ngroups][DW]
     int* tg = comp + ngrp * DWr;                                    // [ngroups]
