@@ -728,8 +728,10 @@ __device__ __forceinline__ uint64_t step_range(const RP& p, int64_t s) {
 // whose offset would leave the 16 candidates (more rejections than candidates).
 constexpr int WD = 16;
 
-// (1024 threads; every thread of the CTA calls it)
-__device__ void randk_walk_body(const RP& p, const uint32_t* words, int64_t nwords, int64_t base0, int64_t t00) {
+// (1024 threads; every thread of the CTA calls it).  Walks positions [base0, pos_end) (pos_end a
+// multiple of 32, or past the stream) from entering offset t00; returns the exit offset.
+__device__ int64_t randk_walk_body(const RP& p, const uint32_t* words, int64_t nwords, int64_t base0, int64_t t00,
+                                   int64_t pos_end) {
   __shared__ uint32_t smask[32][WD];
   __shared__ uint8_t sF[32][WD];
   __shared__ int s_enter[33];
@@ -743,7 +745,7 @@ __device__ void randk_walk_body(const RP& p, const uint32_t* words, int64_t nwor
   uint32_t pf = pf_pos < nwords ? words[pf_pos] : draw32(ph, (uint64_t)pf_pos);
   while (true) {
     const int64_t base = s_base, t0 = s_t0;
-    if (base - t0 >= p.k) break;  // every step has its draw
+    if (base - t0 >= p.k || base >= pos_end) break;  // every step has its draw / the range is walked
     const int64_t pos = base + tid;
     const uint32_t w32 = pos == pf_pos ? pf : (pos < nwords ? words[pos] : draw32(ph, (uint64_t)pos));
     pf_pos = pos + 1024;
@@ -812,7 +814,7 @@ __device__ void randk_walk_body(const RP& p, const uint32_t* words, int64_t nwor
       s_enter[lane] = enter;  // entering offset of warp `lane` (valid for lane <= nw)
       if (lane == 0) {
         s_enter[32] = d;
-        s_nw = nw;
+        s_nw = (int)imin(nw, (pos_end - base) >> 5);  // stop at pos_end
       }
     }
     __syncthreads();
@@ -863,10 +865,13 @@ __device__ void randk_walk_body(const RP& p, const uint32_t* words, int64_t nwor
     }
     __syncthreads();
   }
+  const int64_t t_exit = s_t0;
+  __syncthreads();  // before a next call's thread 0 rewrites s_base / s_t0
+  return t_exit;
 }
 
 __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words, int64_t nwords) {
-  randk_walk_body(p, words, nwords, 0, 0);
+  randk_walk_body(p, words, nwords, 0, 0, INT64_MAX);
 }
 
 // ---- multi-SM draw walk ------------------------------------------------------------------
@@ -1227,7 +1232,49 @@ __global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words
     ctl->fail_t0 = s_ft0;
   }
   __syncthreads();
-  if (s_fb >= 0) randk_walk_body(p, words, nwords, s_fb, s_ft0);  // > 6 sd excursion (rare)
+  if (s_fb >= 0) {
+    // the walk left a window's speculated range (a > 6 sd excursion, or a band capped at DW): walk
+    // serially only the windows whose exact entering offset lies outside their band, and resolve
+    // every other one by its table as soon as the walk is back inside (emit_draws then emits those;
+    // the serially walked ones are marked tin = -1, their draws already written)
+    __shared__ int64_t s_w, s_t;
+    __shared__ int s_mode;
+    if (tid == 0) { s_w = s_fb / WP; s_t = s_ft0; }
+    __syncthreads();
+    while (true) {
+      if (tid == 0) {
+        int64_t w = s_w, t = s_t;
+        int mode = 0;  // 0: every step served; 1: walk window w serially; 2: walk past the last window
+        while (true) {
+          if (w * WP - t >= p.k) break;
+          if (w >= nwin) { mode = 2; break; }
+          const unsigned c = (unsigned)(t - (int)Lw[w]);
+          const int r = c < (unsigned)DW ? (int)tables[w * DW + c] : 255;
+          if (r == 255) { mode = 1; break; }
+          tin[w] = t;
+          t += r;
+          ++w;
+        }
+        s_w = w;
+        s_t = t;
+        s_mode = mode;
+      }
+      __syncthreads();
+      const int mode = s_mode;
+      const int64_t w = s_w, t = s_t;
+      __syncthreads();
+      if (mode == 0) break;
+      const int64_t tout = randk_walk_body(p, words, nwords, w * WP, t, mode == 1 ? (w + 1) * WP : INT64_MAX);
+      if (tid == 0) {
+        if (mode == 1) tin[w] = -1;
+        s_w = w + 1;
+        s_t = tout;
+      }
+      __syncthreads();
+      if (mode == 2) break;
+    }
+    if (tid == 0) ctl->nwin_used = imin(s_w, nwin);
+  }
 }
 
 template <int RX>
@@ -1239,6 +1286,7 @@ __global__ void __launch_bounds__(1024, 2) k_randk_emit_draws(RP p, const uint32
   if (w >= ctl->nwin_used) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t0 = tin[w];
+  if (t0 < 0) return;  // walked serially by the link kernel's fallback
   const int64_t pos = w * WP + tid;
   const uint32_t w32 = words[pos];  // written by the tables kernel for every window position
   for (int i = tid; i < RX * 32; i += blockDim.x) (&smask[0][0])[i] = 0u;
