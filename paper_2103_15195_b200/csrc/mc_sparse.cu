@@ -1422,6 +1422,54 @@ template <bool EF, bool MOM, bool VEC>
 __device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uint32_t* s_words, const uint32_t* s_rank,
                                           uint16_t* s_off, float* s_val, bool stage, bool& bad) {
   const Prologue& pro = p.pro;
+  if constexpr (!EF && !MOM && VEC) {
+    // stateless codec on aligned buffers: U float4 groups of the gradient loaded before any is
+    // processed (U loads in flight per thread: the pass is latency-bound at one; the output may
+    // alias g, but every element is read before its own store and the groups are disjoint)
+    constexpr int U = 4, NG = TB * 4 * 8;
+    for (int i0 = threadIdx.x; i0 < NG; i0 += U * TB) {
+      float4 gv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = e_base + 4 * (int64_t)(i0 + u * TB);
+        gv[u] = (i0 + u * TB < NG && e + 3 < p.n) ? __ldcs(reinterpret_cast<const float4*>(pro.g + e))
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * TB;
+        const int64_t e = e_base + 4 * (int64_t)i;
+        if (i >= NG || e >= p.n) break;
+        const uint32_t wd = s_words[i >> 3];
+        const int sh = (i & 7) * 4;
+        const uint32_t sel4 = (wd >> sh) & 0xfu;
+        uint32_t rk = stage ? s_rank[i >> 3] + __popc(wd & ((1u << sh) - 1u)) : 0u;
+        const bool full = e + 3 < p.n;
+        float w[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+        if (!full)
+          for (int q = 0; q < 4; ++q) w[q] = e + q < p.n ? pro.g[e + q] : 0.0f;
+        float o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bad |= !isfinite(w[q]);
+          const bool sel = (sel4 >> q) & 1u;
+          const float v = p.unbiased ? __fmul_rn(w[q], p.scale) : w[q];
+          o[q] = sel ? __fadd_rn(0.0f, v) : 0.0f;
+          if (stage && sel) {
+            s_off[rk] = (uint16_t)(4 * i + q);
+            s_val[rk] = v;
+            ++rk;
+          }
+        }
+        if (p.out) {
+          if (full) *reinterpret_cast<float4*>(p.out + e) = make_float4(o[0], o[1], o[2], o[3]);
+          else
+            for (int q = 0; q < 4 && e + q < p.n; ++q) p.out[e + q] = o[q];
+        }
+      }
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < TB * 4 * 8; i += blockDim.x) {  // float4 groups, coalesced
     const int64_t e = e_base + 4 * (int64_t)i;
     if (e >= p.n) break;
