@@ -991,9 +991,9 @@ __global__ void __launch_bounds__(1024, DW <= 512 ? 2 : 1) k_randk_tables(RP p, 
   const Philox ph = randk_philox(p);
   if (tid == 128) {
     // expected offset at the window start and its variance (closed form; they only centre and
-    // size the speculated range — the chain checks it).  The range is +-(6 sd + 16), at most
+    // size the speculated range — the chain checks it).  The range is +-(5 sd + 16), at most
     // DW: early windows, whose offset is still nearly deterministic, evaluate a few dozen
-    // entering offsets instead of DW.  A > 6 sd excursion (p ~ 2e-9 per window) hands the rest
+    // entering offsets instead of DW.  A > 5 sd excursion (p ~ 6e-7 per window) hands the rest
     // of the stream to the serial walker: slower, never wrong.  (Warp 4 computes this while
     // warps 0-3 generate the window's draw words.)
     double t, vv;
@@ -1233,7 +1233,7 @@ __global__ void __launch_bounds__(1024) k_randk_link(RP p, const uint32_t* words
   }
   __syncthreads();
   if (s_fb >= 0) {
-    // the walk left a window's speculated range (a > 6 sd excursion, or a band capped at DW): walk
+    // the walk left a window's speculated range (a > 5 sd excursion, or a band capped at DW): walk
     // serially only the windows whose exact entering offset lies outside their band, and resolve
     // every other one by its table as soon as the walk is back inside (emit_draws then emits those;
     // the serially walked ones are marked tin = -1, their draws already written)
@@ -1875,7 +1875,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
   p.tail_shuffle = (n > 10000 && k > n / 50) ? 1 : 0;
   {  // MC_RANDK_BAND_SIGMA: test knob (a narrow band forces the serial fallback; results never change)
     const char* e = getenv("MC_RANDK_BAND_SIGMA");
-    p.band_sig = e ? (float)atof(e) : 6.0f;
+    p.band_sig = e ? (float)atof(e) : 5.0f;  // +-5 sd: an excursion past it (p ~ 6e-7 per window) only costs time
   }
   p.out = out;
   p.payload = a.payload;
