@@ -1548,12 +1548,18 @@ __device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uin
 }
 
 template <bool EF, bool MOM, bool VEC>
-__global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
+// Persistent: a grid of (SMs x resident CTAs) takes tiles in ticket order until all are done
+// (a tile waits in its look-back only on tiles whose tickets were taken earlier, by resident
+// CTAs), so the last partial wave of a 782-tile ResNet-50 grid does not idle most SMs.
+__global__ void __launch_bounds__(TB) k_randk_emit(RP p, int64_t ntiles) {
   __shared__ uint32_t s_words[TB * 4], s_rank[TB * 4];
   __shared__ uint16_t s_off[RK_STAGE];
   __shared__ float s_val[RK_STAGE];
   __shared__ uint64_t s_pre;
+  bool bad = false;
+  for (;;) {
   const int64_t bid = take_ticket(p.w.ticket);
+  if (bid >= ntiles) break;
   if (bid == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   const int64_t nw = cdiv(p.n, 32);
   const int64_t w0 = bid * TB * 4 + (int64_t)threadIdx.x * 4;  // 4 words (128 elements) per thread
@@ -1577,7 +1583,6 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
   }
   const int64_t e_base = bid * TB * 4 * 32;
   const bool stage = total <= RK_STAGE;
-  bool bad = false;
   if (stage) {
     if (threadIdx.x == 0) st_volatile(&p.w.status[bid], (bid == 0 ? LB_PRE : LB_AGG) | total);  // early
     __syncthreads();
@@ -1611,6 +1616,8 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p) {
     }
     __syncthreads();  // every selected value was read before the pass overwrites the state
     rk_stream<EF, MOM, VEC>(p, e_base, s_words, s_rank, s_off, s_val, false, bad);
+  }
+  __syncthreads();  // the tile's shared state (ticket, words, staging) is reused by the next one
   }
   flag(p.err, bad, MC_ERR_NONFINITE);
 }
@@ -1857,6 +1864,18 @@ RandkStats randk_stats(int64_t n, int64_t k, bool tail_shuffle) {
   return RandkStats{sqrt((double)var), best};
 }
 
+// persistent grid of the emit: every resident CTA slot (occupancy queried once per kernel)
+template <typename K>
+unsigned rk_grid(K* kernel, int64_t ntiles) {
+  static std::atomic<int> occ{0};
+  int o = occ.load(std::memory_order_relaxed);
+  if (o == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, TB, 0) != cudaSuccess || o < 1) o = 1;
+    occ.store(o, std::memory_order_relaxed);
+  }
+  return (unsigned)imax(1, imin(ntiles, (int64_t)sm_count() * o));
+}
+
 int encode_randk(const EncodeArgs& a, float* out) {
   const int64_t n = a.n, k = top_k_count(a.spec->sparsity, n);
   RP p{};
@@ -1965,9 +1984,9 @@ int encode_randk(const EncodeArgs& a, float* out) {
   }
   const unsigned ge = (unsigned)cdiv(nwords, TB * 4);
   note_launch();
-#define MC_RK_EMIT(EF, MOM)                                                 \
-  if (vec) k_randk_emit<EF, MOM, true><<<ge, TB, 0, st>>>(p);               \
-  else k_randk_emit<EF, MOM, false><<<ge, TB, 0, st>>>(p);
+#define MC_RK_EMIT(EF, MOM)                                                                      \
+  if (vec) k_randk_emit<EF, MOM, true><<<rk_grid(k_randk_emit<EF, MOM, true>, ge), TB, 0, st>>>(p, ge); \
+  else k_randk_emit<EF, MOM, false><<<rk_grid(k_randk_emit<EF, MOM, false>, ge), TB, 0, st>>>(p, ge);
   if (p.pro.r && p.pro.m) { MC_RK_EMIT(true, true) }
   else if (p.pro.r) { MC_RK_EMIT(true, false) }
   else if (p.pro.m) { MC_RK_EMIT(false, true) }
