@@ -1417,6 +1417,7 @@ __global__ void k_bitmap_all(RP p) {
 // published, so nobody waits; the pairs then go out as coalesced rows.  A CTA selecting more
 // than RK_STAGE elements (dense randk) resolves first and writes them from the bitmap before
 // streaming (its values must be read before the pass overwrites the state).
+constexpr int RKW = 2;  // bitmap words per emit thread: 16384-element tiles (finer tail balance)
 constexpr int RK_STAGE = 2048;  // 1% randk stages ~330 per CTA; denser CTAs write from the bitmap
 template <bool EF, bool MOM, bool VEC>
 __device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uint32_t* s_words, const uint32_t* s_rank,
@@ -1426,7 +1427,7 @@ __device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uin
     // stateless codec on aligned buffers: U float4 groups of the gradient loaded before any is
     // processed (U loads in flight per thread: the pass is latency-bound at one; the output may
     // alias g, but every element is read before its own store and the groups are disjoint)
-    constexpr int U = 4, NG = TB * 4 * 8;
+    constexpr int U = 4, NG = TB * RKW * 8;
     for (int i0 = threadIdx.x; i0 < NG; i0 += U * TB) {
       float4 gv[U];
 #pragma unroll
@@ -1470,7 +1471,7 @@ __device__ __forceinline__ void rk_stream(const RP& p, int64_t e_base, const uin
     }
     return;
   }
-  for (int i = threadIdx.x; i < TB * 4 * 8; i += blockDim.x) {  // float4 groups, coalesced
+  for (int i = threadIdx.x; i < TB * RKW * 8; i += blockDim.x) {  // float4 groups, coalesced
     const int64_t e = e_base + 4 * (int64_t)i;
     if (e >= p.n) break;
     const uint32_t wd = s_words[i >> 3];
@@ -1552,7 +1553,7 @@ template <bool EF, bool MOM, bool VEC>
 // (a tile waits in its look-back only on tiles whose tickets were taken earlier, by resident
 // CTAs), so the last partial wave of a 782-tile ResNet-50 grid does not idle most SMs.
 __global__ void __launch_bounds__(TB) k_randk_emit(RP p, int64_t ntiles) {
-  __shared__ uint32_t s_words[TB * 4], s_rank[TB * 4];
+  __shared__ uint32_t s_words[TB * RKW], s_rank[TB * RKW];
   __shared__ uint16_t s_off[RK_STAGE];
   __shared__ float s_val[RK_STAGE];
   __shared__ uint64_t s_pre;
@@ -1562,11 +1563,11 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p, int64_t ntiles) {
   if (bid >= ntiles) break;
   if (bid == 0 && threadIdx.x == 0) *reinterpret_cast<mc_payload_header*>(p.payload) = p.hdr;
   const int64_t nw = cdiv(p.n, 32);
-  const int64_t w0 = bid * TB * 4 + (int64_t)threadIdx.x * 4;  // 4 words (128 elements) per thread
-  uint32_t words[4];
+  const int64_t w0 = bid * TB * RKW + (int64_t)threadIdx.x * RKW;  // RKW words (32 RKW elements) per thread
+  uint32_t words[RKW];
   uint32_t cnt = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < RKW; ++q) {
     words[q] = (w0 + q < nw) ? p.w.bitmap[w0 + q] : 0u;
     cnt += __popc(words[q]);
   }
@@ -1575,13 +1576,13 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p, int64_t ntiles) {
   {
     uint32_t rk = (uint32_t)ex;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      s_words[threadIdx.x * 4 + q] = words[q];
-      s_rank[threadIdx.x * 4 + q] = rk;
+    for (int q = 0; q < RKW; ++q) {
+      s_words[threadIdx.x * RKW + q] = words[q];
+      s_rank[threadIdx.x * RKW + q] = rk;
       rk += __popc(words[q]);
     }
   }
-  const int64_t e_base = bid * TB * 4 * 32;
+  const int64_t e_base = bid * TB * RKW * 32;
   const bool stage = total <= RK_STAGE;
   if (stage) {
     if (threadIdx.x == 0) st_volatile(&p.w.status[bid], (bid == 0 ? LB_PRE : LB_AGG) | total);  // early
@@ -1601,7 +1602,7 @@ __global__ void __launch_bounds__(TB) k_randk_emit(RP p, int64_t ntiles) {
     const uint64_t pre = block_lookback(p.w.status, bid, total);
     uint64_t pos = pre + ex;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < RKW; ++q) {
       uint32_t m = words[q];
       while (m) {
         const int b = __ffs(m) - 1;
@@ -1904,7 +1905,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
   p.hdr.n_idx = p.hdr.n_val = p.hdr.cap = (uint32_t)k;
   cudaStream_t st = a.ctx.stream;
   const int64_t nwords = cdiv(n, 32);
-  const int64_t nblk = cdiv(nwords, TB * 4) + 1;
+  const int64_t nblk = cdiv(nwords, TB * RKW) + 1;
   const bool vec = (uintptr_t)p.pro.g % 16 == 0 && (!out || (uintptr_t)out % 16 == 0) &&
                    (!p.pro.r || (uintptr_t)p.pro.r % 16 == 0) && (!p.pro.m || (uintptr_t)p.pro.m % 16 == 0);
   auto memsets = [&]() -> int {
@@ -1982,7 +1983,7 @@ int encode_randk(const EncodeArgs& a, float* out) {
       note_launch(); k_randk_floyd_mark<<<gk, 256, 0, st>>>(p);
     }
   }
-  const unsigned ge = (unsigned)cdiv(nwords, TB * 4);
+  const unsigned ge = (unsigned)cdiv(nwords, TB * RKW);
   note_launch();
 #define MC_RK_EMIT(EF, MOM)                                                                      \
   if (vec) k_randk_emit<EF, MOM, true><<<rk_grid(k_randk_emit<EF, MOM, true>, ge), TB, 0, st>>>(p, ge); \
