@@ -1758,8 +1758,10 @@ int encode_topk(const EncodeArgs& a, float* out) {
     set_error("top-k group of %lld elements exceeds the supported %lld", (long long)n, (long long)(H3_MAX_TILES * CB));
     return MC_EINVAL;
   }
-  // zero histograms + ctl + ticket + status in one memset (contiguous in the carve)
-  const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (ntiles + 1);
+  // one memset for the histograms, control words, and the final pass's ticket + look-back
+  // status (passes 1-3 use neither ticket nor status)
+  const int64_t ftiles = cdiv(n, CB_F);
+  const size_t zbytes = (size_t)((uint8_t*)p.w.status - (uint8_t*)p.w.hist) + 8 * (imax(ntiles, ftiles) + 1);
   MC_API_CHECK(cudaMemsetAsync(p.w.hist, 0, zbytes, st));
   const unsigned g1 = (unsigned)imax(1, imin(cdiv(n, 1024), (int64_t)sm_count() * 8));
   note_launch(); k_topk_pass1<<<g1, 256, 0, st>>>(p);
@@ -1768,9 +1770,6 @@ int encode_topk(const EncodeArgs& a, float* out) {
   static std::atomic<uint64_t> h3_cfg{0};  // per device: the opt-in (to the largest table) is set
   if (h3smem > 48 * 1024) MC_API_CHECK(smem_optin(h3_cfg, k_topk_hist3, 4 * (int)(H3_MAX_TILES + 1)));
   note_launch(); k_topk_hist3<<<(unsigned)sm_count() * 2, 256, h3smem, st>>>(p, ntiles);
-  // reset ticket + status for the final look-back pass (list length <= n)
-  const int64_t ftiles = cdiv(n, CB_F);
-  MC_API_CHECK(cudaMemsetAsync(p.w.ticket, 0, 16 + 8 * (ftiles + 1), st));
   note_launch(); k_topk_final<<<(unsigned)imax(1, imin(ftiles, (int64_t)sm_count() * 4)), 256, 0, st>>>(p);
   MC_LAUNCH_CHECK();
   return MC_OK;
