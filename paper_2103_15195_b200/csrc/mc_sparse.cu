@@ -878,13 +878,15 @@ __global__ void __launch_bounds__(1024) k_randk_walk(RP p, const uint32_t* words
 // The draw stream is cut into windows of WP = 1024 positions.  The offset t (rejections so
 // far) at a window's start is unknown, but it is close to its expectation E_w (the sum of the
 // per-draw rejection probabilities ((2^32 - excl) mod excl) / 2^32 before the window):
-//   tables  one CTA per window evaluates the window for every entering offset
-//           t in [L_w, L_w + DW) with L_w = E_w - DW/2 (rejection masks for all offsets
-//           in smem, then one thread per candidate walks them) -> rejections r_w(t);
-//   chain   one CTA composes t_{w+1} = t_w + r_w(t_w) (one smem lookup per window);
+//   tables  one CTA per window evaluates the window for every entering offset t in
+//           [L_w, L_w + dwin), centred on E_w, dwin = 2 (5 sd_w + 16) <= DW (rejection masks
+//           for all offsets in smem, then one thread per candidate walks them) -> r_w(t);
+//   link    groups of 16 windows compose their tables in parallel, the last CTA chains the
+//           groups t_{g+1} = comp_g(t_g) and replays every window's exact entering offset;
 //   emit    one CTA per window re-walks from its exact t_w and writes draws[step];
-//   fallback if t_w ever leaves [L_w, L_w + DW) (a > 7 sigma excursion) the single-CTA
-//           walker finishes the stream from that window.
+//   fallback if t_w ever leaves its window's range (a > 5 sd excursion, or a band capped at
+//           DW), the link kernel's last CTA walks serially the windows outside their
+//           ranges and resolves the others by their tables.
 constexpr int WP = 1024;
 // RX: most rejections one 1024-position window may hold (tables entries and the emit
 // re-walk).  A draw for range excl is rejected with p < excl / 2^32, so a window averages
@@ -892,7 +894,7 @@ constexpr int WP = 1024;
 // DW (speculated entering offsets per window) is 512, or 1024 when the walk's drift is
 // large: the offset's deviation from its expectation is a sum of Bernoulli rejections with
 // sd ~ sqrt(k * (n - k/2) / 2^33) (149 for a 138M-element group at 1%), and a window range
-// of +-DW/2 must cover it or the serial walker takes over
+// of +-DW/2 must cover it or the serial fallback takes over
 
 struct WalkCtl {
   int64_t fail_base, fail_t0;  // fallback start (fail_base < 0: none)
