@@ -127,6 +127,29 @@ def test_derive_seed_native_matches_table(C):
         assert C.derive_seed(root, w, t, g) == (lo | (hi << 64))
 
 
+@pytest.mark.parametrize("sparsity,sigma", [(0.99, None), (0.999, None), (0.99, "2"), (0.98, "3")])
+def test_randk_resnet50_size_matches_oracle(sparsity, sigma, C, monkeypatch):
+    """randk over a whole ResNet-50-sized group (25.56M elements, ~250 windows at 1%): the
+    5-launch path (tables, link, draw emit, Floyd, persistent emit) and, with a narrow band,
+    its hybrid serial fallback — indices and values bit-exact against numpy's choice."""
+    import torch
+
+    import mergecomp_oracle as O
+    from paper_2103_15195_b200.spec import CompressorSpec
+
+    if sigma is not None:
+        monkeypatch.setenv("MC_RANDK_BAND_SIGMA", sigma)
+    n = 25_557_032
+    spec = CompressorSpec("randk", sparsity=sparsity)
+    g = (np.random.default_rng(17).standard_normal(n) * 1e-3).astype(np.float32)
+    seed = O.derive_seed(5, 0, 7, 0)
+    p_dev, _ = C.encode(spec, torch.from_numpy(g).cuda(), None, seed=seed)
+    p_ref, _ = O.encode(spec, g, None, seed=seed)
+    d = p_dev.to_host()
+    assert np.array_equal(np.asarray(d.indices), np.asarray(p_ref.indices))
+    assert np.array_equal(np.asarray(d.values).view(np.uint32), np.asarray(p_ref.values).view(np.uint32))
+
+
 @pytest.mark.parametrize("sigma", ["0", "1.5"])
 def test_randk_serial_fallback_matches_oracle(sigma, C, monkeypatch):
     """A speculated-offset band too narrow for the walk's drift (MC_RANDK_BAND_SIGMA, a test
